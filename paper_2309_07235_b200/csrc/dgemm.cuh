@@ -1,0 +1,273 @@
+// Knob-driven fp64 GEMM for sm_100a:  C (+)= (+/-) A[MxK] * B[KxN]
+//
+// Replaces the reference's matmul_tiled (kernels.cpp:91-111) and serves the
+// LU trailing update (kernels.cpp:205-216) and the Cholesky update
+// (kernels.cpp:273-286, right-looking form, B given as N x K = "NT").
+//
+// Schedule (per CTA, mirrors the reference's (yo, xo) outer tile loops):
+//   * one CTA owns one output REGION of reg_y x reg_x elements — the knob
+//     (fy, fx) of the reference loop nest; sub-atom regions (< 8) are packed
+//     into the 8x8 DMMA atom by the host launcher;
+//   * the region is swept in BM x BN tile steps; each step is a full-K
+//     reduction (the reference's k loop) in BK=16 chunks;
+//   * warp 'NCW' is a TMA producer (one elected lane): each stage is one A box
+//     [BM x 16] and the B box(es), 128B-swizzled, completion on a full
+//     mbarrier; consumer warps release a stage through an empty mbarrier;
+//   * consumer warps own WTM x WTN warp tiles of 8x8x4 DMMA atoms with
+//     register accumulators (fp64 has no TMEM/UMMA path on sm_100a).
+//
+// Bank-conflict-free fragment loads: the k index a lane feeds in DMMA step s
+// is K(s,t) = 8(s>>1) + 2t + (s&1) (so A/B^T pairs are one LDS.128) and the
+// A (and B^T) fragment row g maps to tile row (g>>1) + 4(g&1) inside each
+// 8-row group; with the 128B swizzle every quarter-warp hits 8 distinct
+// 16-byte chunks.  Any permutation of the k order is legal: each output
+// element still receives every product exactly once, accumulated by DMMA.
+#pragma once
+#include <climits>
+#include <cstdint>
+
+#include "tt_ptx.cuh"
+
+namespace tt {
+
+constexpr int kBK = 16;
+
+struct GemmArgs {
+  double* c;       // output view origin: element (0,0) of the M x N view
+  long long ldc;
+  int M, N, K;
+  int a_r0, a_c0;  // A view origin inside the A tensor map (row, col)
+  int b_r0, b_c0;  // NN: (k-row, n-col) of B; NT: (n-row, k-col) of B^T
+  int reg_y, reg_x;
+  int nreg_x;
+  int alpha_neg;   // 1: accumulate -A*B
+  int beta;        // 1: accumulators start from C (C += ...), 0: from zero
+  int lower;       // 1: only write view elements with i + diag_off >= j
+  int diag_off;
+};
+
+template <int BM, int BN, bool BT>
+struct GemmShape {
+  static constexpr int WTM = BM < 32 ? BM : 32;
+  static constexpr int WTN = (BM >= 128 && BN >= 128) ? 64 : (BN < 32 ? BN : 32);
+  static constexpr int WGM = BM / WTM;
+  static constexpr int WGN = BN / WTN;
+  static constexpr int MF = WTM / 8;
+  static constexpr int NF = WTN / 8;
+  static constexpr int NCW = WGM * WGN;
+  static constexpr int THREADS = (NCW + 1) * 32;
+  static constexpr int MAXREG = (65536 / THREADS) / 8 * 8 > 255 ? 255 : (65536 / THREADS) / 8 * 8;
+  static constexpr int STAGES = (BM + BN) >= 192 ? 4 : 6;
+  static constexpr int A_BYTES = BM * kBK * 8;
+  static constexpr int B_COLS = BT ? BN : (BN < 16 ? 16 : BN);  // NN boxes are 16 wide
+  static constexpr int B_BYTES = B_COLS * kBK * 8;
+  static constexpr int NBOX_B = BT ? 1 : B_COLS / 16;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+};
+
+// Byte offset of (row, 16B-chunk) in a tile of 128-byte rows written by TMA
+// with CU_TENSOR_MAP_SWIZZLE_128B (tile base 1024-byte aligned).
+__device__ __forceinline__ int swz(int row, int chunk) {
+  return row * 128 + ((chunk ^ (row & 7)) << 4);
+}
+
+template <int BM, int BN, bool BT>
+__global__ void __maxnreg__((GemmShape<BM, BN, BT>::MAXREG))
+    dgemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                 const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
+  using S = GemmShape<BM, BN, BT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES);
+  uint64_t* empty = full + S::STAGES;
+
+  const int rid = blockIdx.x;
+  const int ry = rid / p.nreg_x;
+  const int rx = rid - ry * p.nreg_x;
+  const int y0 = ry * p.reg_y, x0 = rx * p.reg_x;
+  const int y1 = min(y0 + p.reg_y, p.M), x1 = min(x0 + p.reg_x, p.N);
+  if (p.lower && (y1 - 1 + p.diag_off < x0)) return;  // region strictly above the diagonal
+  const int nty = (y1 - y0 + BM - 1) / BM;
+  const int ntx = (x1 - x0 + BN - 1) / BN;
+  const int nk = (p.K + kBK - 1) / kBK;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < S::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], S::NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == S::NCW) {  // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      prefetch_tmap(&tmB);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int ty = 0; ty < nty; ++ty) {
+        const int ty0 = y0 + ty * BM;
+        const int ty1 = min(ty0 + BM, y1);
+        for (int tx = 0; tx < ntx; ++tx) {
+          const int tx0 = x0 + tx * BN;
+          if (p.lower && (ty1 - 1 + p.diag_off < tx0)) continue;
+          for (int kc = 0; kc < nk; ++kc) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * S::STAGE_BYTES;
+            uint8_t* sb = sa + S::A_BYTES;
+            mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
+            tma_load_2d(sa, &tmA, &full[stage], p.a_c0 + kc * kBK, p.a_r0 + ty0);
+            if (BT) {
+              tma_load_2d(sb, &tmB, &full[stage], p.b_c0 + kc * kBK, p.b_r0 + tx0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < S::NBOX_B; ++j)
+                tma_load_2d(sb + j * (kBK * 128), &tmB, &full[stage], p.b_c0 + tx0 + 16 * j,
+                            p.b_r0 + kc * kBK);
+            }
+            if (++stage == S::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- DMMA consumers ----------------
+  constexpr int MF = S::MF, NF = S::NF;
+  const int wm = warp / S::WGN, wn = warp - (warp / S::WGN) * S::WGN;
+  const int g = lane >> 2, t = lane & 3;
+  const int rperm = (g >> 1) + 4 * (g & 1);
+  const double sgn = p.alpha_neg ? -1.0 : 1.0;
+  int stage = 0;
+  uint32_t phase = 0;
+
+  for (int ty = 0; ty < nty; ++ty) {
+    const int ty0 = y0 + ty * BM;
+    const int ty1 = min(ty0 + BM, y1);
+    for (int tx = 0; tx < ntx; ++tx) {
+      const int tx0 = x0 + tx * BN;
+      if (p.lower && (ty1 - 1 + p.diag_off < tx0)) continue;
+
+      double acc[MF][NF][2];
+#pragma unroll
+      for (int mf = 0; mf < MF; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf) {
+          acc[mf][nf][0] = 0.0;
+          acc[mf][nf][1] = 0.0;
+        }
+      if (p.beta) {
+#pragma unroll
+        for (int mf = 0; mf < MF; ++mf) {
+          const int r = ty0 + wm * S::WTM + mf * 8 + rperm;
+          if (r < ty1) {
+            const double* crow = p.c + static_cast<long long>(r) * p.ldc;
+#pragma unroll
+            for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int cc = tx0 + wn * S::WTN + nf * 8 + (BT ? t + 4 * h : 2 * t + h);
+                if (cc < x1) acc[mf][nf][h] = crow[cc];
+              }
+          }
+        }
+      }
+
+      for (int kc = 0; kc < nk; ++kc) {
+        mbar_wait(&full[stage], phase);
+        const uint8_t* sa = smem + stage * S::STAGE_BYTES;
+        const uint8_t* sb = sa + S::A_BYTES;
+        const bool tail = (p.K - kc * kBK) < kBK;
+        const int kvalid = p.K - kc * kBK;
+
+        // Two k-pairs per chunk: pair sp feeds DMMA steps s = 2sp, 2sp+1 with
+        // k = 8sp + 2t + h.  Large warp tiles keep the pair loop rolled so
+        // only one pair of operand fragments is live next to the accumulators.
+#pragma unroll(S::MF * S::NF >= 32 ? 1 : 2)
+        for (int sp = 0; sp < 2; ++sp) {
+          double a[MF][2];
+#pragma unroll
+          for (int mf = 0; mf < MF; ++mf) {
+            const int row = wm * S::WTM + mf * 8 + rperm;
+            const double2 v = *reinterpret_cast<const double2*>(sa + swz(row, sp * 4 + t));
+            a[mf][0] = v.x * sgn;
+            a[mf][1] = v.y * sgn;
+          }
+          double b[2][NF];
+          if (BT) {
+#pragma unroll
+            for (int nf = 0; nf < NF; ++nf) {
+              const int row = wn * S::WTN + nf * 8 + rperm;
+              const double2 v = *reinterpret_cast<const double2*>(sb + swz(row, sp * 4 + t));
+              b[0][nf] = v.x;
+              b[1][nf] = v.y;
+            }
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int krow = 8 * sp + 2 * t + h;
+#pragma unroll
+              for (int nf = 0; nf < NF; ++nf) {
+                const int cn = wn * S::WTN + nf * 8 + g;
+                const int cc = cn & 15;
+                b[h][nf] = *reinterpret_cast<const double*>(
+                    sb + (cn >> 4) * (kBK * 128) + swz(krow, cc >> 1) + (cc & 1) * 8);
+              }
+            }
+          }
+          if (tail) {  // zero the k >= K lanes of both operands
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (8 * sp + 2 * t + h >= kvalid) {
+#pragma unroll
+                for (int mf = 0; mf < MF; ++mf) a[mf][h] = 0.0;
+#pragma unroll
+                for (int nf = 0; nf < NF; ++nf) b[h][nf] = 0.0;
+              }
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int mf = 0; mf < MF; ++mf)
+#pragma unroll
+              for (int nf = 0; nf < NF; ++nf)
+                dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a[mf][h], b[h][nf]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == S::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+
+      // epilogue: predicated stores inside the region / view / triangle
+#pragma unroll
+      for (int mf = 0; mf < MF; ++mf) {
+        const int r = ty0 + wm * S::WTM + mf * 8 + rperm;
+        if (r < ty1) {
+          double* crow = p.c + static_cast<long long>(r) * p.ldc;
+#pragma unroll
+          for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int cc = tx0 + wn * S::WTN + nf * 8 + (BT ? t + 4 * h : 2 * t + h);
+              if (cc < x1 && (!p.lower || r + p.diag_off >= cc)) crow[cc] = acc[mf][nf][h];
+            }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace tt

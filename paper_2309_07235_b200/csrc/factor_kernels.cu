@@ -1,0 +1,317 @@
+// Panel, triangular-solve, generator and residual kernels for sm_100a.
+//
+// Per-element operation order follows the reference (kernels.cpp): every
+// element receives its rank-1 updates in ascending k, LU multipliers are
+// formed by true division by the pivot, Cholesky off-diagonals are divided
+// by the finished diagonal and diagonals take sqrt after all updates.  The
+// GPU contracts multiply-subtract into DFMA, so parity is by tolerance
+// (north_star: residual <= 1e-12), never by bits — except launch_spd_product,
+// which is bitwise (unfused __dmul_rn/__dadd_rn).
+#include <climits>
+#include <cmath>
+
+#include "factor_kernels.cuh"
+
+namespace tt {
+
+namespace {
+
+constexpr int kPanelThreads = 128;
+
+__device__ __forceinline__ bool failed(const int* info) {
+  return *reinterpret_cast<const volatile int*>(info) != kNoFailure;
+}
+
+// ---------------------------------------------------------------- LU panel
+// Every CTA factors the (w x w) diag block redundantly in shared memory
+// (identical arithmetic, so identical bits); CTA 0 stores it to the scratch
+// block `ws` (writing it into `a` here would race with other CTAs still
+// loading the unfactored block — lu_trsm_u copies it back), and each
+// thread then solves one row below against U11:  for k: x_k /= u_kk;
+// x_j -= x_k * u_kj (j > k)  — kernels.cpp:191-195 for rows i >= q+w.
+__global__ void __launch_bounds__(kPanelThreads) lu_panel_kernel(double* __restrict__ a,
+                                                                 long long ld, int n, int q,
+                                                                 int w, double* __restrict__ ws,
+                                                                 int* info) {
+  __shared__ double D[kIB][kIB + 1];
+  if (failed(info)) return;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < w * w; e += blockDim.x) {
+    const int i = e / w, j = e - (e / w) * w;
+    D[i][j] = a[static_cast<long long>(q + i) * ld + q + j];
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const int i = tid;
+    for (int k = 0; k < w; ++k) {
+      const double piv = D[k][k];
+      if (i == 0 && blockIdx.x == 0 && fabs(piv) < 1e-300) atomicMin(info, q + k);
+      if (i > k && i < w) {
+        const double l = D[i][k] / piv;
+        D[i][k] = l;
+        for (int j = k + 1; j < w; ++j) D[i][j] -= l * D[k][j];
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    for (int e = tid; e < w * w; e += blockDim.x) ws[e] = D[e / w][e - (e / w) * w];
+  }
+  const int row = q + w + blockIdx.x * blockDim.x + tid;
+  if (row >= n) return;
+  double* r = a + static_cast<long long>(row) * ld + q;
+  double x[kIB];
+#pragma unroll
+  for (int j = 0; j < kIB; ++j) x[j] = j < w ? r[j] : 0.0;
+#pragma unroll
+  for (int k = 0; k < kIB; ++k) {
+    if (k < w) {
+      x[k] = x[k] / D[k][k];
+#pragma unroll
+      for (int j = k + 1; j < kIB; ++j)
+        if (j < w) x[j] -= x[k] * D[k][j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kIB; ++j)
+    if (j < w) r[j] = x[j];
+}
+
+// ------------------------------------------------------------ LU U-row solve
+// Column-parallel forward substitution with the unit lower L of the diag
+// block: for k: for i > k: x_i -= l_ik * x_k  (kernels.cpp:198-203).
+__global__ void __launch_bounds__(kPanelThreads) lu_trsm_u_kernel(double* __restrict__ a,
+                                                                  long long ld, int q, int w,
+                                                                  int c0, int ncols,
+                                                                  const double* __restrict__ ws,
+                                                                  const int* info) {
+  __shared__ double L[kIB][kIB + 1];
+  if (failed(info)) return;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < w * w; e += blockDim.x) {
+    const int i = e / w, j = e - (e / w) * w;
+    const double v = ws[e];
+    L[i][j] = v;
+    if (blockIdx.x == 0) a[static_cast<long long>(q + i) * ld + q + j] = v;
+  }
+  __syncthreads();
+  const int col = c0 + blockIdx.x * blockDim.x + tid;
+  if (col >= c0 + ncols) return;
+  double x[kIB];
+#pragma unroll
+  for (int i = 0; i < kIB; ++i) x[i] = i < w ? a[static_cast<long long>(q + i) * ld + col] : 0.0;
+#pragma unroll
+  for (int k = 0; k < kIB; ++k) {
+    if (k < w) {
+#pragma unroll
+      for (int i = k + 1; i < kIB; ++i)
+        if (i < w) x[i] -= L[i][k] * x[k];
+    }
+  }
+#pragma unroll
+  for (int i = 1; i < kIB; ++i)
+    if (i < w) a[static_cast<long long>(q + i) * ld + col] = x[i];
+}
+
+// ----------------------------------------------------------- Cholesky panel
+// Diag block: right-looking potrf in shared memory (per element the same
+// ascending-k updates as the reference's row-oriented loop, kernels.cpp:
+// 289-306); rows below: x_k /= l_kk; x_j -= x_k * l_jk (j > k).
+__global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __restrict__ a,
+                                                                   long long ld, int n, int q,
+                                                                   int w, double* __restrict__ ws,
+                                                                   int* info) {
+  __shared__ double D[kIB][kIB + 1];
+  if (failed(info)) return;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < w * w; e += blockDim.x) {
+    const int i = e / w, j = e - (e / w) * w;
+    D[i][j] = j <= i ? a[static_cast<long long>(q + i) * ld + q + j] : 0.0;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const int i = tid;
+    for (int k = 0; k < w; ++k) {
+      if (i == k) {
+        const double d = D[k][k];
+        if (d <= 0.0 && blockIdx.x == 0) atomicMin(info, q + k);
+        D[k][k] = sqrt(d);
+      }
+      __syncwarp();
+      if (i > k && i < w) D[i][k] = D[i][k] / D[k][k];
+      __syncwarp();
+      if (i > k && i < w) {
+        const double lik = D[i][k];
+        for (int j = k + 1; j <= i; ++j) D[i][j] -= lik * D[j][k];
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    for (int e = tid; e < w * w; e += blockDim.x) ws[e] = D[e / w][e - (e / w) * w];
+  }
+  const int row = q + w + blockIdx.x * blockDim.x + tid;
+  if (row >= n) return;
+  double* r = a + static_cast<long long>(row) * ld + q;
+  double x[kIB];
+#pragma unroll
+  for (int j = 0; j < kIB; ++j) x[j] = j < w ? r[j] : 0.0;
+#pragma unroll
+  for (int k = 0; k < kIB; ++k) {
+    if (k < w) {
+      x[k] = x[k] / D[k][k];
+#pragma unroll
+      for (int j = k + 1; j < kIB; ++j)
+        if (j < w) x[j] -= x[k] * D[j][k];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kIB; ++j)
+    if (j < w) r[j] = x[j];
+}
+
+// Copies the factored diag block from scratch into `a` (lower part only for
+// Cholesky: the upper triangle is never written, kernels.cpp:264-308).
+__global__ void diag_writeback_kernel(double* __restrict__ a, long long ld, int q, int w,
+                                     const double* __restrict__ ws, int lower_only) {
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int i = e / w, j = e - (e / w) * w;
+    if (!lower_only || j <= i) a[static_cast<long long>(q + i) * ld + q + j] = ws[e];
+  }
+}
+
+// ------------------------------------------------- gen_spd product (bitwise)
+// a(i,j) = a(j,i) = sum_k b(i,k)*b(j,k) in ascending k from 0.0, unfused;
+// a(i,i) += n.  16x16 output tile per CTA (lower-triangle tiles only),
+// b rows staged through shared memory.
+constexpr int kSpdT = 16, kSpdK = 32;
+__global__ void __launch_bounds__(kSpdT* kSpdT) spd_product_kernel(const double* __restrict__ b,
+                                                                   long long ldb, int n,
+                                                                   double* __restrict__ a,
+                                                                   long long lda) {
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if (bj > bi) return;
+  __shared__ double Bi[kSpdT][kSpdK + 1];
+  __shared__ double Bj[kSpdT][kSpdK + 1];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int i = bi * kSpdT + ty, j = bj * kSpdT + tx;
+  double s = 0.0;
+  for (int k0 = 0; k0 < n; k0 += kSpdK) {
+    for (int e = ty * kSpdT + tx; e < kSpdT * kSpdK; e += kSpdT * kSpdT) {
+      const int r = e / kSpdK, c = e - (e / kSpdK) * kSpdK;
+      const int gi = bi * kSpdT + r, gj = bj * kSpdT + r, gk = k0 + c;
+      Bi[r][c] = (gi < n && gk < n) ? b[static_cast<long long>(gi) * ldb + gk] : 0.0;
+      Bj[r][c] = (gj < n && gk < n) ? b[static_cast<long long>(gj) * ldb + gk] : 0.0;
+    }
+    __syncthreads();
+    const int kend = min(kSpdK, n - k0);
+    for (int k = 0; k < kend; ++k) s = __dadd_rn(s, __dmul_rn(Bi[ty][k], Bj[tx][k]));
+    __syncthreads();
+  }
+  if (i < n && j < n && j <= i) {
+    if (i == j) {
+      a[static_cast<long long>(i) * lda + i] = __dadd_rn(s, static_cast<double>(n));
+    } else {
+      a[static_cast<long long>(i) * lda + j] = s;
+      a[static_cast<long long>(j) * lda + i] = s;
+    }
+  }
+}
+
+// ------------------------------------------------------------- residual aux
+__global__ void unpack_lu_kernel(const double* __restrict__ f, long long ldf, int n,
+                                 double* __restrict__ l, double* __restrict__ u, long long ld) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<long long>(n) * n) return;
+  const int i = static_cast<int>(idx / n), j = static_cast<int>(idx % n);
+  const double v = f[static_cast<long long>(i) * ldf + j];
+  l[static_cast<long long>(i) * ld + j] = j < i ? v : (j == i ? 1.0 : 0.0);
+  u[static_cast<long long>(i) * ld + j] = j >= i ? v : 0.0;
+}
+
+__global__ void lower_of_kernel(const double* __restrict__ f, long long ldf, int n,
+                                double* __restrict__ l, long long ld) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<long long>(n) * n) return;
+  const int i = static_cast<int>(idx / n), j = static_cast<int>(idx % n);
+  l[static_cast<long long>(i) * ld + j] = j <= i ? f[static_cast<long long>(i) * ldf + j] : 0.0;
+}
+
+__global__ void maxdiff_kernel(const double* __restrict__ x, long long ldx,
+                               const double* __restrict__ y, long long ldy, int rows, int cols,
+                               unsigned long long* out) {
+  double md = 0.0, my = 0.0;
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(idx / cols), j = static_cast<int>(idx % cols);
+    const double yv = y[static_cast<long long>(i) * ldy + j];
+    const double d = fabs(x[static_cast<long long>(i) * ldx + j] - yv);
+    md = d > md ? d : (d != d ? d : md);  // keep NaN visible
+    my = fabs(yv) > my ? fabs(yv) : my;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double od = __shfl_xor_sync(0xffffffffu, md, o);
+    const double oy = __shfl_xor_sync(0xffffffffu, my, o);
+    md = od > md ? od : (od != od ? od : md);
+    my = oy > my ? oy : my;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&out[0], static_cast<unsigned long long>(__double_as_longlong(md)));
+    atomicMax(&out[1], static_cast<unsigned long long>(__double_as_longlong(my)));
+  }
+}
+
+unsigned blocks_for(long long work, int per) {
+  long long b = (work + per - 1) / per;
+  return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+void launch_lu_panel(double* a, long long ld, int n, int q, int w, double* ws, int* info,
+                     cudaStream_t s) {
+  lu_panel_kernel<<<blocks_for(n - q - w, kPanelThreads), kPanelThreads, 0, s>>>(a, ld, n, q, w,
+                                                                               ws, info);
+}
+
+void launch_lu_trsm_u(double* a, long long ld, int q, int w, int c0, int ncols, const double* ws,
+                      const int* info, cudaStream_t s) {
+  // Always launched: CTA 0 also writes the factored diag block back.
+  lu_trsm_u_kernel<<<blocks_for(ncols, kPanelThreads), kPanelThreads, 0, s>>>(
+      a, ld, q, w, c0, ncols < 0 ? 0 : ncols, ws, info);
+}
+
+void launch_chol_panel(double* a, long long ld, int n, int q, int w, double* ws, int* info,
+                       cudaStream_t s) {
+  chol_panel_kernel<<<blocks_for(n - q - w, kPanelThreads), kPanelThreads, 0, s>>>(a, ld, n, q,
+                                                                                 w, ws, info);
+  diag_writeback_kernel<<<1, 256, 0, s>>>(a, ld, q, w, ws, 1);
+}
+
+void launch_spd_product(const double* b, long long ldb, int n, double* a, long long lda,
+                        cudaStream_t s) {
+  const int nb = (n + kSpdT - 1) / kSpdT;
+  spd_product_kernel<<<dim3(nb, nb), dim3(kSpdT, kSpdT), 0, s>>>(b, ldb, n, a, lda);
+}
+
+void launch_unpack_lu(const double* f, long long ldf, int n, double* l, double* u, long long ld,
+                      cudaStream_t s) {
+  unpack_lu_kernel<<<blocks_for(static_cast<long long>(n) * n, 256), 256, 0, s>>>(f, ldf, n, l, u,
+                                                                                ld);
+}
+
+void launch_lower_of(const double* f, long long ldf, int n, double* l, long long ld,
+                     cudaStream_t s) {
+  lower_of_kernel<<<blocks_for(static_cast<long long>(n) * n, 256), 256, 0, s>>>(f, ldf, n, l,
+                                                                               ld);
+}
+
+void launch_maxdiff(const double* x, long long ldx, const double* y, long long ldy, int rows,
+                    int cols, unsigned long long* out, cudaStream_t s) {
+  maxdiff_kernel<<<1184, 256, 0, s>>>(x, ldx, y, ldy, rows, cols, out);
+}
+
+}  // namespace tt

@@ -1,0 +1,104 @@
+// Host side of the DMMA GEMM: TMA descriptor cache, knob -> variant plan,
+// launch.  See gemm.hpp.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "gemm.hpp"
+
+namespace tt {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int tile_edge(int reg) {
+  for (int t : {8, 16, 32, 64}) {
+    if (reg <= t) return t;
+  }
+  return 128;
+}
+
+// Sub-atom knob regions (< 8) are packed: a CTA owns ceil(8/f) adjacent knob
+// regions so that it fills one 8-wide DMMA atom.
+int pack_region(int f, int extent) {
+  int r = f < 8 ? f * ((8 + f - 1) / f) : f;
+  return std::max(1, std::min(r, extent));
+}
+
+}  // namespace
+
+const CUtensorMap* TmapCache::get(const double* base, int rows, int cols, long long ld,
+                                  int box_rows) {
+  auto key = std::make_tuple(static_cast<const void*>(base), rows, cols, ld, box_rows);
+  auto it = maps_.find(key);
+  if (it != maps_.end()) return &it->second;
+  auto fn = encode_fn();
+  if (!fn) return nullptr;
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(double)};
+  cuuint32_t box[2] = {16u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return nullptr;
+  return &maps_.emplace(key, m).first->second;
+}
+
+GemmPlan plan_gemm(int M, int N, int fy, int fx) {
+  GemmPlan p;
+  p.reg_y = pack_region(fy, M);
+  p.reg_x = pack_region(fx, N);
+  p.bm = tile_edge(p.reg_y);
+  p.bn = tile_edge(p.reg_x);
+  p.nreg_y = (M + p.reg_y - 1) / p.reg_y;
+  p.nreg_x = (N + p.reg_x - 1) / p.reg_x;
+  return p;
+}
+
+cudaError_t gemm(TmapCache& tc, const Operand& A, const Operand& B, bool b_trans, double* c,
+                 long long ldc, int M, int N, int K, int fy, int fx, int alpha_neg, int beta,
+                 int lower, int diag_off, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  const GemmPlan plan = plan_gemm(M, N, fy, fx);
+  const CUtensorMap* ta = tc.get(A.base, A.rows, A.cols, A.ld, plan.bm);
+  const CUtensorMap* tb = b_trans ? tc.get(B.base, B.rows, B.cols, B.ld, plan.bn)
+                                  : tc.get(B.base, B.rows, B.cols, B.ld, 16);
+  if (!ta || !tb) return cudaErrorInvalidValue;
+  GemmArgs args;
+  args.c = c;
+  args.ldc = ldc;
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  args.a_r0 = A.r0;
+  args.a_c0 = A.c0;
+  args.b_r0 = B.r0;
+  args.b_c0 = B.c0;
+  args.reg_y = plan.reg_y;
+  args.reg_x = plan.reg_x;
+  args.nreg_x = plan.nreg_x;
+  args.alpha_neg = alpha_neg;
+  args.beta = beta;
+  args.lower = lower;
+  args.diag_off = diag_off;
+  return b_trans ? launch_nt(plan.bm, plan.bn, *ta, *tb, args, plan.grid(), stream)
+                 : launch_nn(plan.bm, plan.bn, *ta, *tb, args, plan.grid(), stream);
+}
+
+}  // namespace tt

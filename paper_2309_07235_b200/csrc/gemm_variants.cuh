@@ -1,0 +1,44 @@
+// Instantiation helper for the AOT DMMA GEMM family.
+#pragma once
+#include "gemm.hpp"
+
+namespace tt {
+
+template <int BM, int BN, bool BT>
+cudaError_t launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args,
+                           long long grid, cudaStream_t stream) {
+  using S = GemmShape<BM, BN, BT>;
+  static bool configured = false;  // per-variant attribute set once per process
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<BM, BN, BT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (grid <= 0) return cudaSuccess;
+  dgemm_kernel<BM, BN, BT><<<static_cast<unsigned>(grid), S::THREADS, S::SMEM, stream>>>(ta, tb,
+                                                                                         args);
+  return cudaGetLastError();
+}
+
+#define TT_DISPATCH_BN(BM, BT)                                                  \
+  switch (bn) {                                                                 \
+    case 8: return launch_variant<BM, 8, BT>(ta, tb, args, grid, stream);       \
+    case 16: return launch_variant<BM, 16, BT>(ta, tb, args, grid, stream);     \
+    case 32: return launch_variant<BM, 32, BT>(ta, tb, args, grid, stream);     \
+    case 64: return launch_variant<BM, 64, BT>(ta, tb, args, grid, stream);     \
+    case 128: return launch_variant<BM, 128, BT>(ta, tb, args, grid, stream);   \
+  }                                                                             \
+  return cudaErrorInvalidValue;
+
+#define TT_DISPATCH(BT)                      \
+  switch (bm) {                              \
+    case 8: { TT_DISPATCH_BN(8, BT) }        \
+    case 16: { TT_DISPATCH_BN(16, BT) }      \
+    case 32: { TT_DISPATCH_BN(32, BT) }      \
+    case 64: { TT_DISPATCH_BN(64, BT) }      \
+    case 128: { TT_DISPATCH_BN(128, BT) }    \
+  }                                          \
+  return cudaErrorInvalidValue;
+
+}  // namespace tt

@@ -1,0 +1,91 @@
+"""CPU tests of the boundary: the C-ABI library loads and exports every symbol
+include/tt_gpu.h declares; the product never routes through the oracle and has
+no CPU fallback; the host-side harness semantics match harness_test.cpp."""
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2309_07235_b200 import _lib, kernels
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "tt_gpu.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|uint64_t)\s+(tt_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_expected_surface():
+    syms = declared_symbols()
+    assert set(syms) == set(_lib.EXPORTS)
+    for must in ("tt_lu_factor_inplace", "tt_cholesky_factor_inplace", "tt_mm3_tiled",
+                 "tt_measure", "tt_ctx_create"):
+        assert must in syms
+
+
+def test_library_loads_and_exports_everything():
+    lib = _lib.load()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert b"sm_100a" in lib.tt_build_info()
+
+
+def test_sm100a_cubin_only():
+    """The .so carries sm_100a SASS (DMMA + TMA), nothing for other archs."""
+    import shutil
+    import subprocess
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+    sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True,
+                          text=True).stdout
+    assert "DMMA" in sass and "UTMALDG" in sass
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    assert lib.tt_ctx_create(0, ctypes.byref(h)) == _lib.TT_EDEVICE
+    with pytest.raises(kernels.DeviceError):
+        kernels.Context(0)
+
+
+def test_product_never_imports_the_oracle():
+    pkg = ROOT / "paper_2309_07235_b200"
+    for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")):
+        text = f.read_text()
+        assert not re.search(r"^\s*(import|from)\s+oracle", text, re.M), f
+        assert "liboracle" not in text and "libtiletuner_ref" not in text, f
+
+
+def test_aggregate_samples_order_statistics():
+    # harness_test.cpp:64-77
+    s = [3.0, 1.0, 2.0, 8.0]
+    assert kernels.aggregate_samples(s, "min") == 1.0
+    assert kernels.aggregate_samples(s, "median") == 2.5
+    assert kernels.aggregate_samples(s, "mean") == 3.5
+    assert kernels.aggregate_samples([5.0, 1.0, 9.0], "median") == 5.0
+    with pytest.raises(ValueError):
+        kernels.aggregate_samples([], "median")
+
+
+def test_env_override(monkeypatch):
+    # harness_test.cpp:79-89
+    base = kernels.MeasureProtocol()
+    monkeypatch.setenv("TILETUNER_REPS", "5")
+    assert kernels.apply_env_overrides(base).repetitions == 5
+    for bad in ("abc", "0", "5 ", "-2", ""):
+        monkeypatch.setenv("TILETUNER_REPS", bad)
+        assert kernels.apply_env_overrides(base).repetitions == base.repetitions, bad
+    monkeypatch.setenv("TILETUNER_REPS", " +7")
+    assert kernels.apply_env_overrides(base).repetitions == 7
+    monkeypatch.delenv("TILETUNER_REPS")
+    assert kernels.apply_env_overrides(base).repetitions == base.repetitions
