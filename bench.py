@@ -257,7 +257,9 @@ def run_gpu_arm(args, rank, world, local):
     n = BENCH_N
     by, bx = BENCH_LU_BLOCK
     ld = n  # 2000 is a multiple of 16: rows already 128-byte aligned
-    stream = torch.cuda.current_stream()
+    # one explicit stream shared by torch (events, copies) and the library
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     sptr = ctypes.c_void_p(stream.cuda_stream)
 
     # inputs: gen_spd(2000, 1) generated on the device (bitwise the reference's)
@@ -274,7 +276,16 @@ def run_gpu_arm(args, rank, world, local):
                            sptr)
         ctx.check(rc)
 
-    launches0 = ctx.launches
+    # Instantiation cache: a schedule's CUDA graph is specific to its buffer,
+    # so build the graph of every ring entry first (untimed), then restore the
+    # pristine inputs and evict them from L2 with a 256 MB write.
+    for i in range(ring_len):
+        factor(i)
+    torch.cuda.synchronize()
+    ring.copy_(base.expand(ring_len, n, ld))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    flush.fill_(1)
+    torch.cuda.synchronize()
     for i in range(args.warmup):
         factor(i)
     torch.cuda.synchronize()
@@ -331,7 +342,7 @@ def run_gpu_arm(args, rank, world, local):
             "data": "synthetic: gen_spd(2000, seed=1) generated on the device, bitwise equal to the reference generator",
             "config": {"workload": f"lu_nopiv_large_n{n}_fixed_block", "n": n, "by": by, "bx": bx,
                        "parallelism": f"replicas{world}",
-                       "l2_policy": f"ring of {ring_len} distinct resident inputs (32 MB each); every step's input cold in L2"},
+                       "l2_policy": f"ring of {ring_len} distinct resident inputs (32 MB each), 256 MB L2 flush after restoring them; every timed step's input is cold in L2"},
             "pct_of_fp64_peak": 100.0 * achieved / FP64_PEAK_TFLOPS,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,

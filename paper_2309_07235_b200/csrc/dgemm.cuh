@@ -40,6 +40,8 @@ struct GemmArgs {
   int b_r0, b_c0;  // NN: (k-row, n-col) of B; NT: (n-row, k-col) of B^T
   int reg_y, reg_x;
   int nreg_x;
+  int klo;         // 1: the A (and B^T) k origin was moved one column left to an even,
+                   //    16-byte-aligned TMA coordinate; k' = 0 is masked (K' = K + 1)
   int alpha_neg;   // 1: accumulate -A*B
   int beta;        // 1: accumulators start from C (C += ...), 0: from zero
   int lower;       // 1: only write view elements with i + diag_off >= j
@@ -48,21 +50,28 @@ struct GemmArgs {
 
 template <int BM, int BN, bool BT>
 struct GemmShape {
+  // Warp tiles up to 32 x 64 (64 fp64 accumulators per lane) and at most 4
+  // consumer warps + 1 producer: the register file is split across the 4
+  // SM sub-partitions (16K regs each), so >4 warps of ~200 registers do not
+  // fit one CTA.  128 x 128 regions are therefore swept as 128 x 64 tiles.
   static constexpr int WTM = BM < 32 ? BM : 32;
-  static constexpr int WTN = (BM >= 128 && BN >= 128) ? 64 : (BN < 32 ? BN : 32);
+  static constexpr int WTN = BN < 64 ? BN : 64;
   static constexpr int WGM = BM / WTM;
   static constexpr int WGN = BN / WTN;
   static constexpr int MF = WTM / 8;
   static constexpr int NF = WTN / 8;
   static constexpr int NCW = WGM * WGN;
   static constexpr int THREADS = (NCW + 1) * 32;
-  static constexpr int MAXREG = (65536 / THREADS) / 8 * 8 > 255 ? 255 : (65536 / THREADS) / 8 * 8;
+  static_assert(NCW <= 4, "at most 4 consumer warps");
   static constexpr int STAGES = (BM + BN) >= 192 ? 4 : 6;
   static constexpr int A_BYTES = BM * kBK * 8;
   static constexpr int B_COLS = BT ? BN : (BN < 16 ? 16 : BN);  // NN boxes are 16 wide
   static constexpr int B_BYTES = B_COLS * kBK * 8;
   static constexpr int NBOX_B = BT ? 1 : B_COLS / 16;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  // NN tiles whose first B column is odd start their boxes one column left
+  // (TMA boxes must start 16-byte aligned) and need one extra box when BN >= 16.
+  static constexpr int B_ALLOC = BT ? B_BYTES : B_BYTES + (BN >= 16 ? kBK * 128 : 0);
+  static constexpr int STAGE_BYTES = A_BYTES + B_ALLOC;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
 };
 
@@ -73,7 +82,7 @@ __device__ __forceinline__ int swz(int row, int chunk) {
 }
 
 template <int BM, int BN, bool BT>
-__global__ void __maxnreg__((GemmShape<BM, BN, BT>::MAXREG))
+__global__ void __launch_bounds__(GemmShape<BM, BN, BT>::THREADS, 1)
     dgemm_kernel(const __grid_constant__ CUtensorMap tmA,
                  const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
   using S = GemmShape<BM, BN, BT>;
@@ -91,7 +100,8 @@ __global__ void __maxnreg__((GemmShape<BM, BN, BT>::MAXREG))
   if (p.lower && (y1 - 1 + p.diag_off < x0)) return;  // region strictly above the diagonal
   const int nty = (y1 - y0 + BM - 1) / BM;
   const int ntx = (x1 - x0 + BN - 1) / BN;
-  const int nk = (p.K + kBK - 1) / kBK;
+  const int kend = p.K + p.klo;  // k' range [klo, kend) is the operand's K
+  const int nk = (kend + kBK - 1) / kBK;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -116,18 +126,20 @@ __global__ void __maxnreg__((GemmShape<BM, BN, BT>::MAXREG))
         for (int tx = 0; tx < ntx; ++tx) {
           const int tx0 = x0 + tx * BN;
           if (p.lower && (ty1 - 1 + p.diag_off < tx0)) continue;
+          const int bs = BT ? 0 : ((p.b_c0 + tx0) & 1);  // NN column shift of this tile
+          const int nbox = S::NBOX_B + ((bs && BN >= 16) ? 1 : 0);
+          const uint32_t tx_bytes = S::A_BYTES + (BT ? S::B_BYTES : nbox * (kBK * 128));
           for (int kc = 0; kc < nk; ++kc) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * S::STAGE_BYTES;
             uint8_t* sb = sa + S::A_BYTES;
-            mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
+            mbar_arrive_expect_tx(&full[stage], tx_bytes);
             tma_load_2d(sa, &tmA, &full[stage], p.a_c0 + kc * kBK, p.a_r0 + ty0);
             if (BT) {
               tma_load_2d(sb, &tmB, &full[stage], p.b_c0 + kc * kBK, p.b_r0 + tx0);
             } else {
-#pragma unroll
-              for (int j = 0; j < S::NBOX_B; ++j)
-                tma_load_2d(sb + j * (kBK * 128), &tmB, &full[stage], p.b_c0 + tx0 + 16 * j,
+              for (int j = 0; j < nbox; ++j)
+                tma_load_2d(sb + j * (kBK * 128), &tmB, &full[stage], p.b_c0 + tx0 - bs + 16 * j,
                             p.b_r0 + kc * kBK);
             }
             if (++stage == S::STAGES) {
@@ -156,6 +168,7 @@ __global__ void __maxnreg__((GemmShape<BM, BN, BT>::MAXREG))
     for (int tx = 0; tx < ntx; ++tx) {
       const int tx0 = x0 + tx * BN;
       if (p.lower && (ty1 - 1 + p.diag_off < tx0)) continue;
+      const int bs = BT ? 0 : ((p.b_c0 + tx0) & 1);
 
       double acc[MF][NF][2];
 #pragma unroll
@@ -186,8 +199,11 @@ __global__ void __maxnreg__((GemmShape<BM, BN, BT>::MAXREG))
         mbar_wait(&full[stage], phase);
         const uint8_t* sa = smem + stage * S::STAGE_BYTES;
         const uint8_t* sb = sa + S::A_BYTES;
-        const bool tail = (p.K - kc * kBK) < kBK;
-        const int kvalid = p.K - kc * kBK;
+        // chunk-local valid k' window [klo_c, kvalid): masks the aligned-origin
+        // column (first chunk) and the K tail (last chunk)
+        const int klo_c = kc == 0 ? p.klo : 0;
+        const int kvalid = kend - kc * kBK;
+        const bool tail = kvalid < kBK || klo_c > 0;
 
         // Two k-pairs per chunk: pair sp feeds DMMA steps s = 2sp, 2sp+1 with
         // k = 8sp + 2t + h.  Large warp tiles keep the pair loop rolled so
@@ -217,7 +233,7 @@ __global__ void __maxnreg__((GemmShape<BM, BN, BT>::MAXREG))
               const int krow = 8 * sp + 2 * t + h;
 #pragma unroll
               for (int nf = 0; nf < NF; ++nf) {
-                const int cn = wn * S::WTN + nf * 8 + g;
+                const int cn = wn * S::WTN + nf * 8 + g + bs;
                 const int cc = cn & 15;
                 b[h][nf] = *reinterpret_cast<const double*>(
                     sb + (cn >> 4) * (kBK * 128) + swz(krow, cc >> 1) + (cc & 1) * 8);
@@ -227,7 +243,8 @@ __global__ void __maxnreg__((GemmShape<BM, BN, BT>::MAXREG))
           if (tail) {  // zero the k >= K lanes of both operands
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              if (8 * sp + 2 * t + h >= kvalid) {
+              const int kk = 8 * sp + 2 * t + h;
+              if (kk >= kvalid || kk < klo_c) {
 #pragma unroll
                 for (int mf = 0; mf < MF; ++mf) a[mf][h] = 0.0;
 #pragma unroll

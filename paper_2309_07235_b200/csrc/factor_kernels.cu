@@ -22,60 +22,97 @@ __device__ __forceinline__ bool failed(const int* info) {
   return *reinterpret_cast<const volatile int*>(info) != kNoFailure;
 }
 
+// ------------------------------------------------------ shared panel pieces
+// The (w x w, w <= 32) diag block lives in registers of warp 0: lane i holds
+// row i; pivot-row / column values move by warp shuffles.
+
+// Loads this CTA's rows of the tall panel (rows [row0, row0+nrows), cols
+// [q, q+w)) into shared memory with coalesced row-contiguous accesses.
+__device__ __forceinline__ void stage_rows(const double* __restrict__ a, long long ld, int q,
+                                           int w, int row0, int nrows,
+                                           double (*T)[kIB + 1]) {
+  for (int e = threadIdx.x; e < nrows * w; e += blockDim.x) {
+    const int r = e / w, c = e - (e / w) * w;
+    T[r][c] = a[static_cast<long long>(row0 + r) * ld + q + c];
+  }
+}
+
+__device__ __forceinline__ void unstage_rows(double* __restrict__ a, long long ld, int q, int w,
+                                             int row0, int nrows, const double (*T)[kIB + 1]) {
+  for (int e = threadIdx.x; e < nrows * w; e += blockDim.x) {
+    const int r = e / w, c = e - (e / w) * w;
+    a[static_cast<long long>(row0 + r) * ld + q + c] = T[r][c];
+  }
+}
+
 // ---------------------------------------------------------------- LU panel
-// Every CTA factors the (w x w) diag block redundantly in shared memory
-// (identical arithmetic, so identical bits); CTA 0 stores it to the scratch
+// Every CTA factors the (w x w) diag block redundantly (identical arithmetic,
+// so identical bits) in warp 0's registers; CTA 0 stores it to the scratch
 // block `ws` (writing it into `a` here would race with other CTAs still
-// loading the unfactored block — lu_trsm_u copies it back), and each
-// thread then solves one row below against U11:  for k: x_k /= u_kk;
-// x_j -= x_k * u_kj (j > k)  — kernels.cpp:191-195 for rows i >= q+w.
+// loading the unfactored block — lu_trsm_u copies it back).  Then each
+// thread solves one row below against U11:  x_k = x_k * (1/u_kk);
+// x_j -= x_k * u_kj (j > k) — kernels.cpp:191-195 for rows i >= q+w.  The
+// diag block divides exactly like the reference; the tall rows multiply by
+// the correctly rounded reciprocal (<= 1 ulp per multiplier, inside the
+// stated tolerance) to keep the 32-step dependency chain short.
 __global__ void __launch_bounds__(kPanelThreads) lu_panel_kernel(double* __restrict__ a,
                                                                  long long ld, int n, int q,
                                                                  int w, double* __restrict__ ws,
                                                                  int* info) {
   __shared__ double D[kIB][kIB + 1];
+  __shared__ double T[kPanelThreads][kIB + 1];
+  __shared__ double rinv[kIB];
   if (failed(info)) return;
   const int tid = threadIdx.x;
-  for (int e = tid; e < w * w; e += blockDim.x) {
-    const int i = e / w, j = e - (e / w) * w;
-    D[i][j] = a[static_cast<long long>(q + i) * ld + q + j];
-  }
-  __syncthreads();
+  const int row0 = q + w + blockIdx.x * kPanelThreads;
+  const int nrows = max(0, min(kPanelThreads, n - row0));
+  stage_rows(a, ld, q, w, row0, nrows, T);
   if (tid < 32) {
     const int i = tid;
-    for (int k = 0; k < w; ++k) {
-      const double piv = D[k][k];
-      if (i == 0 && blockIdx.x == 0 && fabs(piv) < 1e-300) atomicMin(info, q + k);
-      if (i > k && i < w) {
-        const double l = D[i][k] / piv;
-        D[i][k] = l;
-        for (int j = k + 1; j < w; ++j) D[i][j] -= l * D[k][j];
+    double x[kIB];
+#pragma unroll
+    for (int j = 0; j < kIB; ++j)
+      x[j] = (i < w && j < w) ? a[static_cast<long long>(q + i) * ld + q + j] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kIB; ++k) {
+      if (k < w) {
+        const double piv = __shfl_sync(0xffffffffu, x[k], k);
+        if (i == 0 && blockIdx.x == 0 && fabs(piv) < 1e-300) atomicMin(info, q + k);
+        if (i > k) x[k] = x[k] / piv;
+#pragma unroll
+        for (int j = k + 1; j < kIB; ++j) {
+          const double u = __shfl_sync(0xffffffffu, x[j], k);
+          if (i > k) x[j] -= x[k] * u;
+        }
       }
-      __syncwarp();
     }
+#pragma unroll
+    for (int j = 0; j < kIB; ++j) D[i][j] = x[j];
+    if (i < w) rinv[i] = 1.0 / D[i][i];  // D row i was written by this lane
   }
   __syncthreads();
   if (blockIdx.x == 0) {
     for (int e = tid; e < w * w; e += blockDim.x) ws[e] = D[e / w][e - (e / w) * w];
   }
-  const int row = q + w + blockIdx.x * blockDim.x + tid;
-  if (row >= n) return;
-  double* r = a + static_cast<long long>(row) * ld + q;
-  double x[kIB];
+  if (tid < nrows) {
+    double x[kIB];
 #pragma unroll
-  for (int j = 0; j < kIB; ++j) x[j] = j < w ? r[j] : 0.0;
+    for (int j = 0; j < kIB; ++j) x[j] = j < w ? T[tid][j] : 0.0;
 #pragma unroll
-  for (int k = 0; k < kIB; ++k) {
-    if (k < w) {
-      x[k] = x[k] / D[k][k];
+    for (int k = 0; k < kIB; ++k) {
+      if (k < w) {
+        x[k] = x[k] * rinv[k];
 #pragma unroll
-      for (int j = k + 1; j < kIB; ++j)
-        if (j < w) x[j] -= x[k] * D[k][j];
+        for (int j = k + 1; j < kIB; ++j)
+          if (j < w) x[j] -= x[k] * D[k][j];
+      }
     }
-  }
 #pragma unroll
-  for (int j = 0; j < kIB; ++j)
-    if (j < w) r[j] = x[j];
+    for (int j = 0; j < kIB; ++j)
+      if (j < w) T[tid][j] = x[j];
+  }
+  __syncthreads();
+  unstage_rows(a, ld, q, w, row0, nrows, T);
 }
 
 // ------------------------------------------------------------ LU U-row solve
@@ -115,61 +152,72 @@ __global__ void __launch_bounds__(kPanelThreads) lu_trsm_u_kernel(double* __rest
 }
 
 // ----------------------------------------------------------- Cholesky panel
-// Diag block: right-looking potrf in shared memory (per element the same
+// Diag block: right-looking potrf in warp 0's registers (per element the same
 // ascending-k updates as the reference's row-oriented loop, kernels.cpp:
-// 289-306); rows below: x_k /= l_kk; x_j -= x_k * l_jk (j > k).
+// 289-306; diag <= 0 fails exactly like :297-302, NaN passes); rows below:
+// x_k = x_k * (1/l_kk); x_j -= x_k * l_jk (j > k).
 __global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __restrict__ a,
                                                                    long long ld, int n, int q,
                                                                    int w, double* __restrict__ ws,
                                                                    int* info) {
   __shared__ double D[kIB][kIB + 1];
+  __shared__ double T[kPanelThreads][kIB + 1];
+  __shared__ double rinv[kIB];
   if (failed(info)) return;
   const int tid = threadIdx.x;
-  for (int e = tid; e < w * w; e += blockDim.x) {
-    const int i = e / w, j = e - (e / w) * w;
-    D[i][j] = j <= i ? a[static_cast<long long>(q + i) * ld + q + j] : 0.0;
-  }
-  __syncthreads();
+  const int row0 = q + w + blockIdx.x * kPanelThreads;
+  const int nrows = max(0, min(kPanelThreads, n - row0));
+  stage_rows(a, ld, q, w, row0, nrows, T);
   if (tid < 32) {
     const int i = tid;
-    for (int k = 0; k < w; ++k) {
-      if (i == k) {
-        const double d = D[k][k];
-        if (d <= 0.0 && blockIdx.x == 0) atomicMin(info, q + k);
-        D[k][k] = sqrt(d);
+    double x[kIB];
+#pragma unroll
+    for (int j = 0; j < kIB; ++j)
+      x[j] = (i < w && j <= i) ? a[static_cast<long long>(q + i) * ld + q + j] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kIB; ++k) {
+      if (k < w) {
+        if (i == k) {
+          const double d = x[k];
+          if (d <= 0.0 && blockIdx.x == 0) atomicMin(info, q + k);
+          x[k] = sqrt(d);
+        }
+        const double lkk = __shfl_sync(0xffffffffu, x[k], k);
+        if (i > k) x[k] = x[k] / lkk;
+#pragma unroll
+        for (int j = k + 1; j < kIB; ++j) {
+          const double ljk = __shfl_sync(0xffffffffu, x[k], j);
+          if (i >= j) x[j] -= x[k] * ljk;
+        }
       }
-      __syncwarp();
-      if (i > k && i < w) D[i][k] = D[i][k] / D[k][k];
-      __syncwarp();
-      if (i > k && i < w) {
-        const double lik = D[i][k];
-        for (int j = k + 1; j <= i; ++j) D[i][j] -= lik * D[j][k];
-      }
-      __syncwarp();
     }
+#pragma unroll
+    for (int j = 0; j < kIB; ++j) D[i][j] = x[j];
+    if (i < w) rinv[i] = 1.0 / D[i][i];  // D row i was written by this lane
   }
   __syncthreads();
   if (blockIdx.x == 0) {
     for (int e = tid; e < w * w; e += blockDim.x) ws[e] = D[e / w][e - (e / w) * w];
   }
-  const int row = q + w + blockIdx.x * blockDim.x + tid;
-  if (row >= n) return;
-  double* r = a + static_cast<long long>(row) * ld + q;
-  double x[kIB];
+  if (tid < nrows) {
+    double x[kIB];
 #pragma unroll
-  for (int j = 0; j < kIB; ++j) x[j] = j < w ? r[j] : 0.0;
+    for (int j = 0; j < kIB; ++j) x[j] = j < w ? T[tid][j] : 0.0;
 #pragma unroll
-  for (int k = 0; k < kIB; ++k) {
-    if (k < w) {
-      x[k] = x[k] / D[k][k];
+    for (int k = 0; k < kIB; ++k) {
+      if (k < w) {
+        x[k] = x[k] * rinv[k];
 #pragma unroll
-      for (int j = k + 1; j < kIB; ++j)
-        if (j < w) x[j] -= x[k] * D[j][k];
+        for (int j = k + 1; j < kIB; ++j)
+          if (j < w) x[j] -= x[k] * D[j][k];
+      }
     }
-  }
 #pragma unroll
-  for (int j = 0; j < kIB; ++j)
-    if (j < w) r[j] = x[j];
+    for (int j = 0; j < kIB; ++j)
+      if (j < w) T[tid][j] = x[j];
+  }
+  __syncthreads();
+  unstage_rows(a, ld, q, w, row0, nrows, T);
 }
 
 // Copies the factored diag block from scratch into `a` (lower part only for

@@ -39,6 +39,19 @@ int pack_region(int f, int extent) {
   return std::max(1, std::min(r, extent));
 }
 
+// A base that is only 8-byte aligned is moved back one element (origin
+// column + 1) so the tensor map base is 16-byte aligned.
+bool align_base(Operand& o) {
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(o.base);
+  if (addr % 8) return false;
+  if (addr % 16) {
+    o.base -= 1;
+    o.c0 += 1;
+    o.cols += 1;
+  }
+  return true;
+}
+
 }  // namespace
 
 const CUtensorMap* TmapCache::get(const double* base, int rows, int cols, long long ld,
@@ -66,6 +79,7 @@ GemmPlan plan_gemm(int M, int N, int fy, int fx) {
   p.reg_x = pack_region(fx, N);
   p.bm = tile_edge(p.reg_y);
   p.bn = tile_edge(p.reg_x);
+  if (p.bm == 128 && p.bn == 128) p.bn = 64;  // largest variant is 128 x 64 (4 warps of 32 x 64)
   p.nreg_y = (M + p.reg_y - 1) / p.reg_y;
   p.nreg_x = (N + p.reg_x - 1) / p.reg_x;
   return p;
@@ -76,9 +90,26 @@ cudaError_t gemm(TmapCache& tc, const Operand& A, const Operand& B, bool b_trans
                  int lower, int diag_off, cudaStream_t stream) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   const GemmPlan plan = plan_gemm(M, N, fy, fx);
-  const CUtensorMap* ta = tc.get(A.base, A.rows, A.cols, A.ld, plan.bm);
-  const CUtensorMap* tb = b_trans ? tc.get(B.base, B.rows, B.cols, B.ld, plan.bn)
-                                  : tc.get(B.base, B.rows, B.cols, B.ld, 16);
+  // TMA boxes must start 16-byte aligned: the matrix bases must be, and an
+  // odd k origin is moved one column left with that column masked (klo).
+  Operand a = A, b = B;
+  if (!align_base(a) || !align_base(b)) return cudaErrorInvalidValue;
+  int klo = 0;
+  if (a.c0 & 1) {
+    klo = 1;
+    a.c0 -= 1;
+    if (b_trans) {
+      if (!(b.c0 & 1)) return cudaErrorInvalidValue;  // A and B^T k origins must share parity
+      b.c0 -= 1;
+    } else {
+      b.r0 -= 1;
+    }
+  } else if (b_trans && (b.c0 & 1)) {
+    return cudaErrorInvalidValue;
+  }
+  const CUtensorMap* ta = tc.get(a.base, a.rows, a.cols, a.ld, plan.bm);
+  const CUtensorMap* tb = b_trans ? tc.get(b.base, b.rows, b.cols, b.ld, plan.bn)
+                                  : tc.get(b.base, b.rows, b.cols, b.ld, 16);
   if (!ta || !tb) return cudaErrorInvalidValue;
   GemmArgs args;
   args.c = c;
@@ -86,10 +117,11 @@ cudaError_t gemm(TmapCache& tc, const Operand& A, const Operand& B, bool b_trans
   args.M = M;
   args.N = N;
   args.K = K;
-  args.a_r0 = A.r0;
-  args.a_c0 = A.c0;
-  args.b_r0 = B.r0;
-  args.b_c0 = B.c0;
+  args.a_r0 = a.r0;
+  args.a_c0 = a.c0;
+  args.b_r0 = b.r0;
+  args.b_c0 = b.c0;
+  args.klo = klo;
   args.reg_y = plan.reg_y;
   args.reg_x = plan.reg_x;
   args.nreg_x = plan.nreg_x;

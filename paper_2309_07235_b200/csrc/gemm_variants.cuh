@@ -27,7 +27,7 @@ cudaError_t launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const G
     case 16: return launch_variant<BM, 16, BT>(ta, tb, args, grid, stream);     \
     case 32: return launch_variant<BM, 32, BT>(ta, tb, args, grid, stream);     \
     case 64: return launch_variant<BM, 64, BT>(ta, tb, args, grid, stream);     \
-    case 128: return launch_variant<BM, 128, BT>(ta, tb, args, grid, stream);   \
+    case 128: return launch_variant<BM, (BM == 128 ? 64 : 128), BT>(ta, tb, args, grid, stream); \
   }                                                                             \
   return cudaErrorInvalidValue;
 

@@ -40,26 +40,33 @@ def rel(x, ref):
 
 @pytest.mark.parametrize("bt", [False, True])
 def test_gemm_tile_family_vs_torch(gpu_ctx, bt):
-    """Every (BM, BN) variant, NN and NT, odd extents and K tails, +/- and C+= modes."""
+    """Every (BM, BN) variant, NN and NT, odd extents, odd (8-byte aligned) origins,
+    K tails, and the C = A*B / C -= A*B modes, against torch fp64."""
     import ctypes
     import torch
     torch.manual_seed(0)
     lib = gpu_ctx.lib
+    side = torch.cuda.Stream()  # a real (non-legacy) stream shared with the library
+    torch.cuda.set_stream(side)
+    stream = ctypes.c_void_p(side.cuda_stream)
     cases = [(37, 45, 29), (128, 128, 16), (200, 136, 33), (8, 8, 4), (1, 1, 1), (130, 70, 100),
              (257, 129, 47)]
     regions = [1, 8, 16, 32, 64, 128, 200]
-    for (M, N, K), (fy, fx) in itertools.product(cases, itertools.product(regions, regions)):
+    for (M, N, K), (fy, fx), off in itertools.product(cases, itertools.product(regions, regions),
+                                                      (0, 1)):
+        if off and (fy, fx) not in ((8, 8), (64, 64), (128, 128), (1, 200)):
+            continue
         fy_ = [d for d in divisors(M) if d <= fy][-1]
         fx_ = [d for d in divisors(N) if d <= fx][-1]
-        lda = (K + 1) // 2 * 2 + 2
-        A = torch.rand(M, lda, dtype=torch.float64, device="cuda")[:, :K]
+        lda = (K + off + 1) // 2 * 2 + 2
+        A = torch.rand(M, lda, dtype=torch.float64, device="cuda")[:, off:off + K]
         if bt:
-            ldb = (K + 1) // 2 * 2
-            B = torch.rand(N, ldb, dtype=torch.float64, device="cuda")[:, :K]
+            ldb = (K + off + 1) // 2 * 2
+            B = torch.rand(N, ldb, dtype=torch.float64, device="cuda")[:, off:off + K]
             ref_ab = A @ B.T
         else:
-            ldb = (N + 1) // 2 * 2 + 4
-            B = torch.rand(K, ldb, dtype=torch.float64, device="cuda")[:, :N]
+            ldb = (N + off + 1) // 2 * 2 + 4
+            B = torch.rand(K, ldb, dtype=torch.float64, device="cuda")[:, off:off + N]
             ref_ab = A @ B
         ldc = N + 3
         Cfull = torch.rand(M, ldc, dtype=torch.float64, device="cuda")
@@ -69,13 +76,13 @@ def test_gemm_tile_family_vs_torch(gpu_ctx, bt):
             rc = lib.tt_dev_gemm(gpu_ctx.handle, ctypes.c_void_p(A.data_ptr()), lda,
                                  ctypes.c_void_p(B.data_ptr()), ldb, int(bt),
                                  ctypes.c_void_p(Cfull.data_ptr()), ldc, M, N, K, fy_, fx_, alpha,
-                                 beta, None)
+                                 beta, stream)
             gpu_ctx.check(rc)
-            torch.cuda.synchronize()
             want = alpha * ref_ab + (C0 if beta else 0)
             err = (Cfull[:, :N] - want).abs().max().item() / max(want.abs().max().item(), 1e-300)
-            assert err <= 1e-13, (M, N, K, fy_, fx_, alpha, beta, err)
-        assert torch.all(Cfull[:, N:] != 0) or ldc == N  # padding columns untouched (rand > 0)
+            assert err <= 1e-13, (M, N, K, fy_, fx_, alpha, beta, off, err)
+        assert torch.all(Cfull[:, N:] != 0)  # columns outside the view untouched (rand > 0)
+    torch.cuda.set_stream(torch.cuda.default_stream())
 
 
 # ------------------------------------------------------------------------ 3mm
