@@ -46,6 +46,11 @@ struct GemmArgs {
   int beta;        // 1: accumulators start from C (C += ...), 0: from zero
   int lower;       // 1: only write view elements with i + diag_off >= j
   int diag_off;
+  int c_tma;       // beta=1 only: the producer TMA-prefetches each tile's C block
+                   // (box BM x (BN+2) from an even column, `c_sh` = view column
+                   // shift of the map) so the accumulator init never waits on
+                   // global-memory latency
+  int c_sh;
 };
 
 template <int BM, int BN, bool BT>
@@ -72,7 +77,9 @@ struct GemmShape {
   // (TMA boxes must start 16-byte aligned) and need one extra box when BN >= 16.
   static constexpr int B_ALLOC = BT ? B_BYTES : B_BYTES + (BN >= 16 ? kBK * 128 : 0);
   static constexpr int STAGE_BYTES = A_BYTES + B_ALLOC;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+  static constexpr int C_LD = BN + 2;  // doubles per row of the C prefetch box
+  static constexpr int C_BYTES = BM * C_LD * 8;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + C_BYTES + 2 * STAGES * 8 + 16 + 1024;
 };
 
 // Byte offset of (row, 16B-chunk) in a tile of 128-byte rows written by TMA
@@ -84,13 +91,18 @@ __device__ __forceinline__ int swz(int row, int chunk) {
 template <int BM, int BN, bool BT>
 __global__ void __launch_bounds__(GemmShape<BM, BN, BT>::THREADS, 1)
     dgemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                 const __grid_constant__ CUtensorMap tmB, const GemmArgs p) {
+                 const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmC, const GemmArgs p) {
   using S = GemmShape<BM, BN, BT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES);
+  double* sC = reinterpret_cast<double*>(smem + S::STAGES * S::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES + S::C_BYTES);
   uint64_t* empty = full + S::STAGES;
+  uint64_t* cfull = empty + S::STAGES;
+  uint64_t* cempty = cfull + 1;
+  const bool c_tma = p.beta && p.c_tma;
 
   const int rid = blockIdx.x;
   const int ry = rid / p.nreg_x;
@@ -110,6 +122,8 @@ __global__ void __launch_bounds__(GemmShape<BM, BN, BT>::THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], S::NCW);
     }
+    mbar_init(cfull, 1);
+    mbar_init(cempty, S::NCW);
     fence_mbar_init();
   }
   __syncthreads();
@@ -118,14 +132,23 @@ __global__ void __launch_bounds__(GemmShape<BM, BN, BT>::THREADS, 1)
     if (lane == 0) {
       prefetch_tmap(&tmA);
       prefetch_tmap(&tmB);
+      if (c_tma) prefetch_tmap(&tmC);
       int stage = 0;
       uint32_t phase = 0;
+      uint32_t cphase = 0;
       for (int ty = 0; ty < nty; ++ty) {
         const int ty0 = y0 + ty * BM;
         const int ty1 = min(ty0 + BM, y1);
         for (int tx = 0; tx < ntx; ++tx) {
           const int tx0 = x0 + tx * BN;
           if (p.lower && (ty1 - 1 + p.diag_off < tx0)) continue;
+          if (c_tma) {  // C block of this tile, once the consumers read the last one
+            mbar_wait(cempty, cphase ^ 1);
+            mbar_arrive_expect_tx(cfull, S::C_BYTES);
+            const int cc0 = p.c_sh + tx0;
+            tma_load_2d(sC, &tmC, cfull, cc0 & ~1, ty0);
+            cphase ^= 1;
+          }
           const int bs = BT ? 0 : ((p.b_c0 + tx0) & 1);  // NN column shift of this tile
           const int nbox = S::NBOX_B + ((bs && BN >= 16) ? 1 : 0);
           const uint32_t tx_bytes = S::A_BYTES + (BT ? S::B_BYTES : nbox * (kBK * 128));
@@ -161,6 +184,7 @@ __global__ void __launch_bounds__(GemmShape<BM, BN, BT>::THREADS, 1)
   const double sgn = p.alpha_neg ? -1.0 : 1.0;
   int stage = 0;
   uint32_t phase = 0;
+  uint32_t cphase = 0;
 
   for (int ty = 0; ty < nty; ++ty) {
     const int ty0 = y0 + ty * BM;
@@ -178,7 +202,24 @@ __global__ void __launch_bounds__(GemmShape<BM, BN, BT>::THREADS, 1)
           acc[mf][nf][0] = 0.0;
           acc[mf][nf][1] = 0.0;
         }
-      if (p.beta) {
+      if (c_tma) {
+        mbar_wait(cfull, cphase);
+        cphase ^= 1;
+        const int cs = (p.c_sh + tx0) & 1;
+#pragma unroll
+        for (int mf = 0; mf < MF; ++mf) {
+          const int rl = wm * S::WTM + mf * 8 + rperm;
+#pragma unroll
+          for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int cl = wn * S::WTN + nf * 8 + (BT ? t + 4 * h : 2 * t + h);
+              acc[mf][nf][h] = sC[rl * S::C_LD + cl + cs];
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(cempty);
+      } else if (p.beta) {
 #pragma unroll
         for (int mf = 0; mf < MF; ++mf) {
           const int r = ty0 + wm * S::WTM + mf * 8 + rperm;

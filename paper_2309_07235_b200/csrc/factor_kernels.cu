@@ -16,210 +16,6 @@ namespace tt {
 
 namespace {
 
-constexpr int kPanelThreads = 128;
-
-__device__ __forceinline__ bool failed(const int* info) {
-  return *reinterpret_cast<const volatile int*>(info) != kNoFailure;
-}
-
-// ------------------------------------------------------ shared panel pieces
-// The (w x w, w <= 32) diag block lives in registers of warp 0: lane i holds
-// row i; pivot-row / column values move by warp shuffles.
-
-// Loads this CTA's rows of the tall panel (rows [row0, row0+nrows), cols
-// [q, q+w)) into shared memory with coalesced row-contiguous accesses.
-__device__ __forceinline__ void stage_rows(const double* __restrict__ a, long long ld, int q,
-                                           int w, int row0, int nrows,
-                                           double (*T)[kIB + 1]) {
-  for (int e = threadIdx.x; e < nrows * w; e += blockDim.x) {
-    const int r = e / w, c = e - (e / w) * w;
-    T[r][c] = a[static_cast<long long>(row0 + r) * ld + q + c];
-  }
-}
-
-__device__ __forceinline__ void unstage_rows(double* __restrict__ a, long long ld, int q, int w,
-                                             int row0, int nrows, const double (*T)[kIB + 1]) {
-  for (int e = threadIdx.x; e < nrows * w; e += blockDim.x) {
-    const int r = e / w, c = e - (e / w) * w;
-    a[static_cast<long long>(row0 + r) * ld + q + c] = T[r][c];
-  }
-}
-
-// ---------------------------------------------------------------- LU panel
-// Every CTA factors the (w x w) diag block redundantly (identical arithmetic,
-// so identical bits) in warp 0's registers; CTA 0 stores it to the scratch
-// block `ws` (writing it into `a` here would race with other CTAs still
-// loading the unfactored block — lu_trsm_u copies it back).  Then each
-// thread solves one row below against U11:  x_k = x_k * (1/u_kk);
-// x_j -= x_k * u_kj (j > k) — kernels.cpp:191-195 for rows i >= q+w.  The
-// diag block divides exactly like the reference; the tall rows multiply by
-// the correctly rounded reciprocal (<= 1 ulp per multiplier, inside the
-// stated tolerance) to keep the 32-step dependency chain short.
-__global__ void __launch_bounds__(kPanelThreads) lu_panel_kernel(double* __restrict__ a,
-                                                                 long long ld, int n, int q,
-                                                                 int w, double* __restrict__ ws,
-                                                                 int* info) {
-  __shared__ double D[kIB][kIB + 1];
-  __shared__ double T[kPanelThreads][kIB + 1];
-  __shared__ double rinv[kIB];
-  if (failed(info)) return;
-  const int tid = threadIdx.x;
-  const int row0 = q + w + blockIdx.x * kPanelThreads;
-  const int nrows = max(0, min(kPanelThreads, n - row0));
-  stage_rows(a, ld, q, w, row0, nrows, T);
-  if (tid < 32) {
-    const int i = tid;
-    double x[kIB];
-#pragma unroll
-    for (int j = 0; j < kIB; ++j)
-      x[j] = (i < w && j < w) ? a[static_cast<long long>(q + i) * ld + q + j] : 0.0;
-#pragma unroll
-    for (int k = 0; k < kIB; ++k) {
-      if (k < w) {
-        const double piv = __shfl_sync(0xffffffffu, x[k], k);
-        if (i == 0 && blockIdx.x == 0 && fabs(piv) < 1e-300) atomicMin(info, q + k);
-        if (i > k) x[k] = x[k] / piv;
-#pragma unroll
-        for (int j = k + 1; j < kIB; ++j) {
-          const double u = __shfl_sync(0xffffffffu, x[j], k);
-          if (i > k) x[j] -= x[k] * u;
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kIB; ++j) D[i][j] = x[j];
-    if (i < w) rinv[i] = 1.0 / D[i][i];  // D row i was written by this lane
-  }
-  __syncthreads();
-  if (blockIdx.x == 0) {
-    for (int e = tid; e < w * w; e += blockDim.x) ws[e] = D[e / w][e - (e / w) * w];
-  }
-  if (tid < nrows) {
-    double x[kIB];
-#pragma unroll
-    for (int j = 0; j < kIB; ++j) x[j] = j < w ? T[tid][j] : 0.0;
-#pragma unroll
-    for (int k = 0; k < kIB; ++k) {
-      if (k < w) {
-        x[k] = x[k] * rinv[k];
-#pragma unroll
-        for (int j = k + 1; j < kIB; ++j)
-          if (j < w) x[j] -= x[k] * D[k][j];
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kIB; ++j)
-      if (j < w) T[tid][j] = x[j];
-  }
-  __syncthreads();
-  unstage_rows(a, ld, q, w, row0, nrows, T);
-}
-
-// ------------------------------------------------------------ LU U-row solve
-// Column-parallel forward substitution with the unit lower L of the diag
-// block: for k: for i > k: x_i -= l_ik * x_k  (kernels.cpp:198-203).
-__global__ void __launch_bounds__(kPanelThreads) lu_trsm_u_kernel(double* __restrict__ a,
-                                                                  long long ld, int q, int w,
-                                                                  int c0, int ncols,
-                                                                  const double* __restrict__ ws,
-                                                                  const int* info) {
-  __shared__ double L[kIB][kIB + 1];
-  if (failed(info)) return;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < w * w; e += blockDim.x) {
-    const int i = e / w, j = e - (e / w) * w;
-    const double v = ws[e];
-    L[i][j] = v;
-    if (blockIdx.x == 0) a[static_cast<long long>(q + i) * ld + q + j] = v;
-  }
-  __syncthreads();
-  const int col = c0 + blockIdx.x * blockDim.x + tid;
-  if (col >= c0 + ncols) return;
-  double x[kIB];
-#pragma unroll
-  for (int i = 0; i < kIB; ++i) x[i] = i < w ? a[static_cast<long long>(q + i) * ld + col] : 0.0;
-#pragma unroll
-  for (int k = 0; k < kIB; ++k) {
-    if (k < w) {
-#pragma unroll
-      for (int i = k + 1; i < kIB; ++i)
-        if (i < w) x[i] -= L[i][k] * x[k];
-    }
-  }
-#pragma unroll
-  for (int i = 1; i < kIB; ++i)
-    if (i < w) a[static_cast<long long>(q + i) * ld + col] = x[i];
-}
-
-// ----------------------------------------------------------- Cholesky panel
-// Diag block: right-looking potrf in warp 0's registers (per element the same
-// ascending-k updates as the reference's row-oriented loop, kernels.cpp:
-// 289-306; diag <= 0 fails exactly like :297-302, NaN passes); rows below:
-// x_k = x_k * (1/l_kk); x_j -= x_k * l_jk (j > k).
-__global__ void __launch_bounds__(kPanelThreads) chol_panel_kernel(double* __restrict__ a,
-                                                                   long long ld, int n, int q,
-                                                                   int w, double* __restrict__ ws,
-                                                                   int* info) {
-  __shared__ double D[kIB][kIB + 1];
-  __shared__ double T[kPanelThreads][kIB + 1];
-  __shared__ double rinv[kIB];
-  if (failed(info)) return;
-  const int tid = threadIdx.x;
-  const int row0 = q + w + blockIdx.x * kPanelThreads;
-  const int nrows = max(0, min(kPanelThreads, n - row0));
-  stage_rows(a, ld, q, w, row0, nrows, T);
-  if (tid < 32) {
-    const int i = tid;
-    double x[kIB];
-#pragma unroll
-    for (int j = 0; j < kIB; ++j)
-      x[j] = (i < w && j <= i) ? a[static_cast<long long>(q + i) * ld + q + j] : 0.0;
-#pragma unroll
-    for (int k = 0; k < kIB; ++k) {
-      if (k < w) {
-        if (i == k) {
-          const double d = x[k];
-          if (d <= 0.0 && blockIdx.x == 0) atomicMin(info, q + k);
-          x[k] = sqrt(d);
-        }
-        const double lkk = __shfl_sync(0xffffffffu, x[k], k);
-        if (i > k) x[k] = x[k] / lkk;
-#pragma unroll
-        for (int j = k + 1; j < kIB; ++j) {
-          const double ljk = __shfl_sync(0xffffffffu, x[k], j);
-          if (i >= j) x[j] -= x[k] * ljk;
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kIB; ++j) D[i][j] = x[j];
-    if (i < w) rinv[i] = 1.0 / D[i][i];  // D row i was written by this lane
-  }
-  __syncthreads();
-  if (blockIdx.x == 0) {
-    for (int e = tid; e < w * w; e += blockDim.x) ws[e] = D[e / w][e - (e / w) * w];
-  }
-  if (tid < nrows) {
-    double x[kIB];
-#pragma unroll
-    for (int j = 0; j < kIB; ++j) x[j] = j < w ? T[tid][j] : 0.0;
-#pragma unroll
-    for (int k = 0; k < kIB; ++k) {
-      if (k < w) {
-        x[k] = x[k] * rinv[k];
-#pragma unroll
-        for (int j = k + 1; j < kIB; ++j)
-          if (j < w) x[j] -= x[k] * D[j][k];
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kIB; ++j)
-      if (j < w) T[tid][j] = x[j];
-  }
-  __syncthreads();
-  unstage_rows(a, ld, q, w, row0, nrows, T);
-}
-
 // Copies the factored diag block from scratch into `a` (lower part only for
 // Cholesky: the upper triangle is never written, kernels.cpp:264-308).
 __global__ void diag_writeback_kernel(double* __restrict__ a, long long ld, int q, int w,
@@ -319,24 +115,9 @@ unsigned blocks_for(long long work, int per) {
 
 }  // namespace
 
-void launch_lu_panel(double* a, long long ld, int n, int q, int w, double* ws, int* info,
-                     cudaStream_t s) {
-  lu_panel_kernel<<<blocks_for(n - q - w, kPanelThreads), kPanelThreads, 0, s>>>(a, ld, n, q, w,
-                                                                               ws, info);
-}
-
-void launch_lu_trsm_u(double* a, long long ld, int q, int w, int c0, int ncols, const double* ws,
-                      const int* info, cudaStream_t s) {
-  // Always launched: CTA 0 also writes the factored diag block back.
-  lu_trsm_u_kernel<<<blocks_for(ncols, kPanelThreads), kPanelThreads, 0, s>>>(
-      a, ld, q, w, c0, ncols < 0 ? 0 : ncols, ws, info);
-}
-
-void launch_chol_panel(double* a, long long ld, int n, int q, int w, double* ws, int* info,
-                       cudaStream_t s) {
-  chol_panel_kernel<<<blocks_for(n - q - w, kPanelThreads), kPanelThreads, 0, s>>>(a, ld, n, q,
-                                                                                 w, ws, info);
-  diag_writeback_kernel<<<1, 256, 0, s>>>(a, ld, q, w, ws, 1);
+void launch_diag_writeback(double* a, long long ld, int q, int w, const double* ws,
+                           int lower_only, cudaStream_t s) {
+  diag_writeback_kernel<<<1, 256, 0, s>>>(a, ld, q, w, ws, lower_only);
 }
 
 void launch_spd_product(const double* b, long long ldb, int n, double* a, long long lda,

@@ -6,10 +6,11 @@
 
 namespace tt {
 
-// Inner blocking width of the panel kernels: a reference panel of width bx
-// is factored as ceil(bx/32) sub-panels, each a diag factorization + row
-// solves + a DMMA update (same per-element operation set).
-constexpr int kIB = 32;
+// Widest panel one fused panel kernel factors: a reference panel of width
+// bx <= 64 is ONE launch; wider panels are factored as ceil(bx/64)
+// sub-panels, each a fused panel + U-row solve + DMMA update (same
+// per-element operation set).
+constexpr int kIB = 64;
 
 // Status word value meaning "no numerical failure" (memset byte 0x7F).
 constexpr int kNoFailure = 0x7F7F7F7F;
@@ -20,14 +21,19 @@ constexpr int kNoFailure = 0x7F7F7F7F;
 void launch_lu_panel(double* a, long long ld, int n, int q, int w, double* ws, int* info,
                      cudaStream_t s);
 // U rows [q, q+w) x cols [c0, c0+ncols): forward substitution with the unit
-// lower L of the sub-panel's diag block (kernels.cpp:198-203).
-// Also copies the factored diag block from `ws` back into `a`.
-void launch_lu_trsm_u(double* a, long long ld, int q, int w, int c0, int ncols, const double* ws,
-                      const int* info, cudaStream_t s);
+// lower L of the sub-panel's diag block (kernels.cpp:198-203), read from
+// `lsrc` (leading dim `lld`: the scratch `ws` with lld = w, or `a` itself).
+// With `writeback` CTA 0 also copies the diag block from `lsrc` into `a`.
+void launch_lu_trsm_u(double* a, long long ld, int q, int w, int c0, int ncols,
+                      const double* lsrc, long long lld, int writeback, const int* info,
+                      cudaStream_t s);
 // Cholesky sub-panel: diag potrf (diag <= 0 fails, kernels.cpp:297-302) +
-// row solves below (kernels.cpp:292-295); lower triangle only.
+// row solves below (kernels.cpp:292-295); lower triangle only.  The factored
+// diag block goes to `ws`; launch_diag_writeback copies it into `a`.
 void launch_chol_panel(double* a, long long ld, int n, int q, int w, double* ws, int* info,
                        cudaStream_t s);
+void launch_diag_writeback(double* a, long long ld, int q, int w, const double* ws,
+                           int lower_only, cudaStream_t s);
 
 // gen_spd on the device, bitwise equal to kernels.cpp:38-55: a = b*b^T + n*I
 // with unfused, ascending-k products (b row-major n x n, ld_b).

@@ -29,11 +29,14 @@ class TmapCache {
   // 2-D fp64 map over the full matrix, box = 16 columns x box_rows rows,
   // 128B swizzle.  Returns nullptr on an encode failure.
   const CUtensorMap* get(const double* base, int rows, int cols, long long ld, int box_rows);
+  // Unswizzled map with an arbitrary (even) box width, for the C prefetch.
+  const CUtensorMap* get_plain(const double* base, int rows, int cols, long long ld, int box_rows,
+                               int box_cols);
   void clear() { maps_.clear(); }
   size_t size() const { return maps_.size(); }
 
  private:
-  std::map<std::tuple<const void*, int, int, long long, int>, CUtensorMap> maps_;
+  std::map<std::tuple<const void*, int, int, long long, int, int>, CUtensorMap> maps_;
 };
 
 // Region (knob) -> launch geometry.  Sub-atom regions are packed into the
@@ -55,8 +58,10 @@ cudaError_t gemm(TmapCache& tc, const Operand& A, const Operand& B, bool b_trans
 
 // Per-variant launchers (gemm_nn.cu / gemm_nt.cu).
 cudaError_t launch_nn(int bm, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
-                      const GemmArgs& args, long long grid, cudaStream_t stream);
+                      const CUtensorMap& tc, const GemmArgs& args, long long grid,
+                      cudaStream_t stream);
 cudaError_t launch_nt(int bm, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
-                      const GemmArgs& args, long long grid, cudaStream_t stream);
+                      const CUtensorMap& tc, const GemmArgs& args, long long grid,
+                      cudaStream_t stream);
 
 }  // namespace tt

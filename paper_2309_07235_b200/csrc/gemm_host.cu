@@ -54,22 +54,41 @@ bool align_base(Operand& o) {
 
 }  // namespace
 
-const CUtensorMap* TmapCache::get(const double* base, int rows, int cols, long long ld,
-                                  int box_rows) {
-  auto key = std::make_tuple(static_cast<const void*>(base), rows, cols, ld, box_rows);
-  auto it = maps_.find(key);
-  if (it != maps_.end()) return &it->second;
+namespace {
+
+bool encode(CUtensorMap* m, const double* base, int rows, int cols, long long ld, int box_rows,
+            int box_cols, bool swizzle) {
   auto fn = encode_fn();
-  if (!fn) return nullptr;
-  CUtensorMap m;
+  if (!fn) return false;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(double)};
-  cuuint32_t box[2] = {16u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1u, 1u};
-  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return nullptr;
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+const CUtensorMap* TmapCache::get(const double* base, int rows, int cols, long long ld,
+                                  int box_rows) {
+  auto key = std::make_tuple(static_cast<const void*>(base), rows, cols, ld, box_rows, 0);
+  auto it = maps_.find(key);
+  if (it != maps_.end()) return &it->second;
+  CUtensorMap m;
+  if (!encode(&m, base, rows, cols, ld, box_rows, 16, true)) return nullptr;
+  return &maps_.emplace(key, m).first->second;
+}
+
+const CUtensorMap* TmapCache::get_plain(const double* base, int rows, int cols, long long ld,
+                                        int box_rows, int box_cols) {
+  auto key = std::make_tuple(static_cast<const void*>(base), rows, cols, ld, box_rows, box_cols);
+  auto it = maps_.find(key);
+  if (it != maps_.end()) return &it->second;
+  CUtensorMap m;
+  if (!encode(&m, base, rows, cols, ld, box_rows, box_cols, false)) return nullptr;
   return &maps_.emplace(key, m).first->second;
 }
 
@@ -129,8 +148,24 @@ cudaError_t gemm(TmapCache& tc, const Operand& A, const Operand& B, bool b_trans
   args.beta = beta;
   args.lower = lower;
   args.diag_off = diag_off;
-  return b_trans ? launch_nt(plan.bm, plan.bn, *ta, *tb, args, plan.grid(), stream)
-                 : launch_nn(plan.bm, plan.bn, *ta, *tb, args, plan.grid(), stream);
+  // C prefetch map (beta = 1): over the M x N view, 16-byte aligned base, an
+  // even leading dimension (TMA stride rule); otherwise plain loads.
+  args.c_tma = 0;
+  args.c_sh = 0;
+  const CUtensorMap* tcm = ta;
+  const uintptr_t caddr = reinterpret_cast<uintptr_t>(c);
+  if (beta && (ldc % 2) == 0 && (caddr % 8) == 0) {
+    const int sh = (caddr % 16) ? 1 : 0;
+    const int bn_eff = plan.bm == 128 && plan.bn == 128 ? 64 : plan.bn;
+    const CUtensorMap* m = tc.get_plain(c - sh, M, N + sh, ldc, plan.bm, bn_eff + 2);
+    if (m) {
+      tcm = m;
+      args.c_tma = 1;
+      args.c_sh = sh;
+    }
+  }
+  return b_trans ? launch_nt(plan.bm, plan.bn, *ta, *tb, *tcm, args, plan.grid(), stream)
+                 : launch_nn(plan.bm, plan.bn, *ta, *tb, *tcm, args, plan.grid(), stream);
 }
 
 }  // namespace tt

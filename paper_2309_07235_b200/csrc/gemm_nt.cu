@@ -3,7 +3,7 @@
 
 namespace tt {
 cudaError_t launch_nt(int bm, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
-                      const GemmArgs& args, long long grid, cudaStream_t stream) {
+                      const CUtensorMap& tc, const GemmArgs& args, long long grid, cudaStream_t stream) {
   TT_DISPATCH(true)
 }
 }  // namespace tt

@@ -5,8 +5,8 @@
 namespace tt {
 
 template <int BM, int BN, bool BT>
-cudaError_t launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args,
-                           long long grid, cudaStream_t stream) {
+cudaError_t launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                           const GemmArgs& args, long long grid, cudaStream_t stream) {
   using S = GemmShape<BM, BN, BT>;
   static bool configured = false;  // per-variant attribute set once per process
   if (!configured) {
@@ -16,18 +16,18 @@ cudaError_t launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const G
     configured = true;
   }
   if (grid <= 0) return cudaSuccess;
-  dgemm_kernel<BM, BN, BT><<<static_cast<unsigned>(grid), S::THREADS, S::SMEM, stream>>>(ta, tb,
+  dgemm_kernel<BM, BN, BT><<<static_cast<unsigned>(grid), S::THREADS, S::SMEM, stream>>>(ta, tb, tc,
                                                                                          args);
   return cudaGetLastError();
 }
 
 #define TT_DISPATCH_BN(BM, BT)                                                  \
   switch (bn) {                                                                 \
-    case 8: return launch_variant<BM, 8, BT>(ta, tb, args, grid, stream);       \
-    case 16: return launch_variant<BM, 16, BT>(ta, tb, args, grid, stream);     \
-    case 32: return launch_variant<BM, 32, BT>(ta, tb, args, grid, stream);     \
-    case 64: return launch_variant<BM, 64, BT>(ta, tb, args, grid, stream);     \
-    case 128: return launch_variant<BM, (BM == 128 ? 64 : 128), BT>(ta, tb, args, grid, stream); \
+    case 8: return launch_variant<BM, 8, BT>(ta, tb, tc, args, grid, stream);       \
+    case 16: return launch_variant<BM, 16, BT>(ta, tb, tc, args, grid, stream);     \
+    case 32: return launch_variant<BM, 32, BT>(ta, tb, tc, args, grid, stream);     \
+    case 64: return launch_variant<BM, 64, BT>(ta, tb, tc, args, grid, stream);     \
+    case 128: return launch_variant<BM, (BM == 128 ? 64 : 128), BT>(ta, tb, tc, args, grid, stream); \
   }                                                                             \
   return cudaErrorInvalidValue;
 

@@ -243,11 +243,11 @@ int factor_graph(tt_ctx* ctx, int kernel, double* a, int n, long long ld, int by
   return get_graph(
       ctx, key,
       [&](tt::ScheduleStats* st) {
+        const tt::Streams ss{ctx->stream, ctx->stream2, ctx->fork, ctx->join};
         return kernel == TT_KERNEL_LU
-                   ? tt::enqueue_lu(ctx->tmaps, a, n, ld, by, bx, ctx->ws, ctx->info,
-                                    ctx->stream, st)
-                   : tt::enqueue_cholesky(ctx->tmaps, a, n, ld, by, bx, ctx->ws, ctx->info,
-                                          ctx->stream, st);
+                   ? tt::enqueue_lu(ctx->tmaps, a, n, ld, by, bx, ctx->ws, ctx->info, ss, st)
+                   : tt::enqueue_cholesky(ctx->tmaps, a, n, ld, by, bx, ctx->ws, ctx->info, ss,
+                                          st);
       },
       g, nodes);
 }
@@ -262,8 +262,8 @@ int mm3_graph(tt_ctx* ctx, const tt::Mm3Bufs& b, const int* d, const int* cfg,
   return get_graph(
       ctx, key,
       [&](tt::ScheduleStats* st) {
-        return tt::enqueue_mm3(ctx->tmaps, b, d[0], d[1], d[2], d[3], d[4], cfg, ctx->stream,
-                               ctx->stream2, ctx->fork, ctx->join, st);
+        const tt::Streams ss{ctx->stream, ctx->stream2, ctx->fork, ctx->join};
+        return tt::enqueue_mm3(ctx->tmaps, b, d[0], d[1], d[2], d[3], d[4], cfg, ss, st);
       },
       g, nodes);
 }
@@ -412,8 +412,8 @@ int tt_ctx_create(int device, tt_ctx** out) {
       for (int bn : {8, 16, 32, 64, 128}) {
         tt::GemmArgs dummy{};
         CUtensorMap m{};
-        cudaError_t r = bt ? tt::launch_nt(bm, bn, m, m, dummy, 0, ctx->stream)
-                           : tt::launch_nn(bm, bn, m, m, dummy, 0, ctx->stream);
+        cudaError_t r = bt ? tt::launch_nt(bm, bn, m, m, m, dummy, 0, ctx->stream)
+                           : tt::launch_nn(bm, bn, m, m, m, dummy, 0, ctx->stream);
         if (r != cudaSuccess) return cleanup(TT_EDEVICE);
       }
   *out = ctx;

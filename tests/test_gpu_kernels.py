@@ -68,7 +68,8 @@ def test_gemm_tile_family_vs_torch(gpu_ctx, bt):
             ldb = (N + off + 1) // 2 * 2 + 4
             B = torch.rand(K, ldb, dtype=torch.float64, device="cuda")[:, off:off + N]
             ref_ab = A @ B
-        ldc = N + 3
+        # even ldc -> TMA-prefetched C (beta=1); odd ldc -> plain C loads
+        ldc = N + (3 if off else (2 if N % 2 == 0 else 3))
         Cfull = torch.rand(M, ldc, dtype=torch.float64, device="cuda")
         C0 = Cfull[:, :N].clone()
         for alpha, beta in ((1, 0), (-1, 1)):
