@@ -12,8 +12,8 @@ from paper_2309_07235_b200 import _lib, kernels
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def declared_symbols():
-    text = (ROOT / "include" / "tt_gpu.h").read_text()
+def declared_symbols(header="tt_gpu.h"):
+    text = (ROOT / "include" / header).read_text()
     return sorted(set(re.findall(r"^\s*(?:int|const char\*|uint64_t)\s+(tt_\w+)\s*\(", text, re.M)))
 
 
@@ -30,6 +30,15 @@ def test_library_loads_and_exports_everything():
     for name in declared_symbols():
         assert hasattr(lib, name), name
     assert b"sm_100a" in lib.tt_build_info()
+
+
+def test_tuner_library_exports_everything():
+    from paper_2309_07235_b200 import tuning
+    lib = tuning.load()
+    syms = declared_symbols("tt_tuner.h")
+    assert len(syms) >= 12
+    for name in syms:
+        assert hasattr(lib, name), name
 
 
 def test_sm100a_cubin_only():

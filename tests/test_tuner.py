@@ -1,0 +1,113 @@
+"""CPU tests of the host tuning runtime (libtt_tuner.so): bit-exact search space,
+reference-identical k=1 tuning traces, and the batch extension's invariants."""
+import pytest
+
+from paper_2309_07235_b200 import tuning
+
+KID = {"lu": 0, "cholesky": 1, "3mm": 2}
+
+
+def test_divisors_match_reference(golden):
+    for key, want in golden["space"].items():
+        if key.startswith("divisors_"):
+            n = int(key.split("_")[1])
+            assert tuning.divisor_candidates(n) == want, n
+    with pytest.raises(ValueError):
+        tuning.divisor_candidates(0)
+
+
+def test_space_sizes_and_table1(golden):
+    # Table 1 of the paper (PAPER.md:155-176 / acceptance_main.cpp:86-103)
+    assert tuning.space_size("3mm", "large") == 74_649_600
+    assert tuning.space_size("3mm", "extralarge") == 228_614_400
+    assert tuning.space_size("lu", "large") == 400
+    assert tuning.space_size("cholesky", "extralarge") == 576
+    for key, want in golden["space"].items():
+        if key.startswith("size_"):
+            _, kern, size = key.split("_", 2)
+            assert tuning.space_size(kern, size) == want, key
+    with pytest.raises(ValueError):
+        tuning.space_size("lu", "huge")
+
+
+def test_config_at_index_of_encode_bit_exact(golden):
+    for key, samples in golden["space"].items():
+        if not key.startswith("samples_"):
+            continue
+        _, kern, size = key.split("_", 2)
+        for s in samples:
+            cfg = tuning.config_at(kern, size, s["flat"])
+            assert list(cfg) == s["config"], (key, s["flat"])
+            assert tuning.index_of(kern, size, cfg) == s["flat"]
+            assert tuning.encode(kern, size, cfg) == s["encode"]  # exact doubles
+    with pytest.raises(ValueError):
+        tuning.index_of("lu", "large", (3, 3))
+
+
+def test_synthetic_objective_optimum():
+    # harness_test.cpp:13-27: optimum (40,40) of lu/large with value exactly 1.0
+    assert tuning.synthetic_objective("lu", "large", (40, 40)) == 1.0
+    import math
+    want = 1.0 + 2.0 * math.log2(40.0) ** 2
+    assert abs(tuning.synthetic_objective("lu", "large", (1, 1)) - want) <= 1e-15 * want
+
+
+@pytest.mark.parametrize("trace", ["lu_large", "cholesky_extralarge", "3mm_mini", "3mm_extralarge"])
+@pytest.mark.parametrize("tuner", ["random", "grid", "bayesopt"])
+def test_k1_trace_equals_reference(golden, trace, tuner):
+    """The batched runtime at k=1 reproduces the reference run_tuning bit for bit."""
+    kern, size = trace.split("_", 1)
+    ref = golden["traces"][f"{kern}_{size}_{tuner}_seed7"]
+    recs, _ = tuning.run_tuning_synthetic(tuner, kern, size, 7, len(ref["flat"]), workers=1)
+    assert [r.flat for r in recs] == ref["flat"]
+    assert [r.runtime_s for r in recs] == ref["runtime"]
+
+
+def test_ask_tell_contract():
+    t = tuning.Tuner("bayesopt", "lu", "mini", 3)
+    a = t.ask_batch(3)
+    assert len(set(a)) == 3
+    with pytest.raises(ValueError):
+        t.tell(10**9, 1.0)  # never asked
+    for f in a:
+        t.tell(f, 1.0 + f * 1e-3)
+    with pytest.raises(ValueError):
+        t.tell(a[0], 1.0)  # told twice
+    seen = set(a)
+    while True:
+        got = t.ask_batch(5)
+        if not got:
+            break
+        assert not (set(got) & seen)
+        seen |= set(got)
+        for f in got:
+            t.tell(f, None if f % 7 == 0 else 2.0)  # failures are penalised, not dropped
+    assert len(seen) == tuning.space_size("lu", "mini")  # exhausted exactly once each
+
+
+@pytest.mark.parametrize("workers", [2, 8])
+def test_batched_invariants_and_speedup(workers):
+    """Async batched evaluator (virtual clock): unique configs, completion order,
+    prefix-min best, and a shorter time-to-best than one evaluator."""
+    k1, _ = tuning.run_tuning_synthetic("bayesopt", "3mm", "extralarge", 11, 120, workers=1)
+    kw, _ = tuning.run_tuning_synthetic("bayesopt", "3mm", "extralarge", 11, 120, workers=workers)
+    assert len(kw) == 120 and len({r.flat for r in kw}) == 120
+    el = [r.elapsed_s for r in kw]
+    assert el == sorted(el)
+    best = float("inf")
+    for r in kw:
+        best = min(best, r.runtime_s)
+        assert r.best_so_far_s == best
+    assert {r.worker for r in kw} == set(range(workers))
+    target = min(r.runtime_s for r in k1)
+    reach = [r.elapsed_s for r in kw if r.runtime_s <= target]
+    t1 = tuning.time_to_best(k1)
+    if reach:  # the batched run found an equally good config: it got there faster
+        assert reach[0] < t1
+    assert kw[-1].elapsed_s < k1[-1].elapsed_s  # same budget, less wall time
+
+
+def test_budget_max_seconds():
+    recs, tot = tuning.run_tuning_synthetic("random", "lu", "large", 1, 400, max_seconds=50.0)
+    assert 0 < len(recs) < 400
+    assert recs[-2].elapsed_s < 50.0  # checked before each evaluation
