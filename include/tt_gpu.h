@@ -132,6 +132,12 @@ int tt_dev_gemm(tt_ctx* ctx, const double* a, int lda, const double* b,
                 int ldb, int b_trans, double* c, int ldc, int M, int N, int K,
                 int fy, int fx, int alpha, int beta, void* stream);
 
+/* Shard-invariant device input generator for the scaled 3mm (no CPU oracle
+ * exists at N = 32768): element (i, j) of rows [row0, row0+rows) of global
+ * matrix `stream_id` is splitmix64(seed, stream_id, row0+i, j) >> 11 * 2^-53. */
+int tt_dev_fill_uniform(tt_ctx* ctx, double* a, int rows, int cols, int ld, long long row0,
+                        uint64_t seed, int stream_id, void* stream);
+
 /* Counter of kernel launches issued by this context (graph nodes count once
  * per graph launch); the bench reports it as gpu_launches. */
 uint64_t tt_launch_count(const tt_ctx* ctx);

@@ -25,7 +25,7 @@ EXPORTS = (
     "tt_lu_factor_inplace", "tt_cholesky_factor_inplace", "tt_mm3_tiled",
     "tt_setup_host", "tt_setup_seeded", "tt_run", "tt_measure", "tt_measure_samples",
     "tt_get_input", "tt_residual", "tt_dev_lu", "tt_dev_cholesky", "tt_dev_mm3",
-    "tt_dev_gemm", "tt_launch_count", "tt_build_info",
+    "tt_dev_gemm", "tt_dev_fill_uniform", "tt_launch_count", "tt_build_info",
 )
 
 _lib = None
@@ -65,6 +65,8 @@ def load() -> ctypes.CDLL:
         "tt_dev_cholesky": (c_int, [vp, vp, c_int, c_int, c_int, c_int, c_int_p, vp]),
         "tt_dev_mm3": (c_int, [vp] + [vp, c_int] * 7 + [c_int] * 5 + [c_int_p, c_int, vp]),
         "tt_dev_gemm": (c_int, [vp, vp, c_int, vp, c_int, c_int, vp, c_int] + [c_int] * 7 + [vp]),
+        "tt_dev_fill_uniform": (c_int, [vp, vp, c_int, c_int, c_int, ctypes.c_longlong,
+                                        ctypes.c_uint64, c_int, vp]),
         "tt_launch_count": (ctypes.c_uint64, [vp]),
         "tt_build_info": (ctypes.c_char_p, []),
     }

@@ -64,6 +64,30 @@ __global__ void __launch_bounds__(kSpdT* kSpdT) spd_product_kernel(const double*
   }
 }
 
+// ------------------------------------------- counter-based U[0,1) (scaled 3mm)
+// x(i, j) = (splitmix64(seed ^ stream * C1 ^ (row0 + i) * C2 ^ j) >> 11) * 2^-53:
+// a pure function of the GLOBAL element index, so a row-sharded matrix is
+// bit-identical to the unsharded one.
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_uniform_kernel(double* __restrict__ a, long long ld, int rows, int cols,
+                                    long long row0, unsigned long long seed, int stream) {
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = idx / cols, j = idx - (idx / cols) * cols;
+    const unsigned long long key = seed ^ (static_cast<unsigned long long>(stream) * 0xD1B54A32D192ED03ULL) ^
+                                   (static_cast<unsigned long long>(row0 + i) * 0x8CB92BA72F3D8DD7ULL) ^
+                                   static_cast<unsigned long long>(j);
+    a[i * ld + j] = static_cast<double>(splitmix64(key) >> 11) * 0x1.0p-53;
+  }
+}
+
 // ------------------------------------------------------------- residual aux
 __global__ void unpack_lu_kernel(const double* __restrict__ f, long long ldf, int n,
                                  double* __restrict__ l, double* __restrict__ u, long long ld) {
@@ -136,6 +160,11 @@ void launch_lower_of(const double* f, long long ldf, int n, double* l, long long
                      cudaStream_t s) {
   lower_of_kernel<<<blocks_for(static_cast<long long>(n) * n, 256), 256, 0, s>>>(f, ldf, n, l,
                                                                                ld);
+}
+
+void launch_fill_uniform(double* a, long long ld, int rows, int cols, long long row0,
+                         unsigned long long seed, int stream, cudaStream_t s) {
+  fill_uniform_kernel<<<1184, 256, 0, s>>>(a, ld, rows, cols, row0, seed, stream);
 }
 
 void launch_maxdiff(const double* x, long long ldx, const double* y, long long ldy, int rows,

@@ -40,6 +40,12 @@ void launch_diag_writeback(double* a, long long ld, int q, int w, const double* 
 void launch_spd_product(const double* b, long long ldb, int n, double* a, long long lda,
                         cudaStream_t s);
 
+// Counter-based U[0,1) fill of rows [row0, row0+rows) of a global matrix
+// (`stream` separates matrices): shard-invariant device inputs for the
+// scaled 3mm, where no CPU oracle exists.
+void launch_fill_uniform(double* a, long long ld, int rows, int cols, long long row0,
+                         unsigned long long seed, int stream, cudaStream_t s);
+
 // Residual helpers.
 void launch_unpack_lu(const double* f, long long ldf, int n, double* l, double* u, long long ld,
                       cudaStream_t s);

@@ -819,6 +819,16 @@ int tt_dev_mm3(tt_ctx* ctx, const double* a, int lda, const double* b, int ldb, 
   return TT_OK;
 }
 
+int tt_dev_fill_uniform(tt_ctx* ctx, double* a, int rows, int cols, int ld, long long row0,
+                        uint64_t seed, int stream_id, void* stream) {
+  if (!ctx || !a || rows < 0 || cols < 0 || ld < cols) return TT_EINVAL;
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  tt::launch_fill_uniform(a, ld, rows, cols, row0, seed, stream_id, s);
+  TT_CUDA(ctx, cudaGetLastError(), "fill_uniform");
+  ctx->launches += 1;
+  return TT_OK;
+}
+
 int tt_dev_gemm(tt_ctx* ctx, const double* a, int lda, const double* b, int ldb, int b_trans,
                 double* c, int ldc, int M, int N, int K, int fy, int fx, int alpha, int beta,
                 void* stream) {

@@ -98,3 +98,22 @@ def test_env_override(monkeypatch):
     assert kernels.apply_env_overrides(base).repetitions == 7
     monkeypatch.delenv("TILETUNER_REPS")
     assert kernels.apply_env_overrides(base).repetitions == base.repetitions
+
+
+def test_cpp_shim_compiles_against_reference_types(tmp_path):
+    """The C++ drop-in (csrc/tiletuner_gpu.hpp) takes tiletuner::Matrix /
+    Configuration and throws the reference's error types."""
+    import shutil
+    import subprocess
+    ref_inc = Path("/root/reference/proj/core/include")
+    if not ref_inc.exists() or not shutil.which("g++"):
+        pytest.skip("reference headers not present (GPU box)")
+    exe = tmp_path / "dropin_demo"
+    cmd = ["g++", "-std=c++20", "-O1", str(ROOT / "examples" / "dropin_demo.cpp"),
+           f"-I{ref_inc}", f"-I{ROOT / 'paper_2309_07235_b200' / 'csrc'}",
+           f"-L{ROOT / 'paper_2309_07235_b200'}", "-ltt_gpu",
+           f"-Wl,-rpath,{ROOT / 'paper_2309_07235_b200'}", "-o", str(exe)]
+    subprocess.run(cmd, check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    import torch
+    assert r.returncode == (0 if torch.cuda.is_available() else 3), r.stdout + r.stderr

@@ -321,3 +321,30 @@ def test_measure_semantics(gpu_ctx):
     fast = big.measure((400, 50), MeasureProtocol(1, 3, "min"))
     assert slow > 2 * fast
     assert gpu_ctx.cache_size >= 3
+
+
+# ------------------------------------------------- scaled 3mm + measured tuning
+
+def test_scaled_mm3_single_gpu_freivalds():
+    from paper_2309_07235_b200.sharded import run_scaled
+    out = run_scaled(n=2048, steps=1, warmup=0, kblocks=8)
+    assert out["freivalds_rel"] <= 1e-10
+    assert out["tflops"] > 0
+
+
+def test_measured_tuning_loop(gpu_ctx):
+    """run_tuning with the GPU objective (spot check, device inputs, BO) on cuda:0."""
+    from paper_2309_07235_b200 import tuning
+    recs, total = tuning.run_tuning_measured("bayesopt", "lu", "small", 5, 14, devices=(0,),
+                                             warmups=1, reps=3)
+    assert len(recs) == 14 and len({r.flat for r in recs}) == 14
+    assert all(r.runtime_s and r.runtime_s > 0 for r in recs)
+    best = float("inf")
+    for r in recs:
+        best = min(best, r.runtime_s)
+        assert r.best_so_far_s == best
+    assert [r.elapsed_s for r in recs] == sorted(r.elapsed_s for r in recs)
+    # two evaluator slots on the same device exercise the asynchronous dispatcher
+    recs2, _ = tuning.run_tuning_measured("bayesopt", "3mm", "small", 5, 16, devices=(0, 0),
+                                          warmups=0, reps=1)
+    assert len(recs2) == 16 and {r.worker for r in recs2} == {0, 1}
