@@ -138,6 +138,13 @@ int tt_dev_gemm(tt_ctx* ctx, const double* a, int lda, const double* b,
 int tt_dev_fill_uniform(tt_ctx* ctx, double* a, int rows, int cols, int ld, long long row0,
                         uint64_t seed, int stream_id, void* stream);
 
+/* Persistent tile-DAG schedule (dag_factor.cu), host-side introspection:
+ * writes up to `cap` tasks as int quadruples {kind | j << 2, k, r0, r1}
+ * (kind 0 DIAG, 1 TRSM_L, 2 TRSM_U, 3 GEMM) and returns the task count, or
+ * -1 when (n, by, bx) runs on the launch-per-kernel graph schedule instead.
+ * Needs no device. */
+int tt_dag_tasks(int kernel, int n, int by, int bx, int* out, int cap);
+
 /* Counter of kernel launches issued by this context (graph nodes count once
  * per graph launch); the bench reports it as gpu_launches. */
 uint64_t tt_launch_count(const tt_ctx* ctx);

@@ -25,7 +25,7 @@ EXPORTS = (
     "tt_lu_factor_inplace", "tt_cholesky_factor_inplace", "tt_mm3_tiled",
     "tt_setup_host", "tt_setup_seeded", "tt_run", "tt_measure", "tt_measure_samples",
     "tt_get_input", "tt_residual", "tt_dev_lu", "tt_dev_cholesky", "tt_dev_mm3",
-    "tt_dev_gemm", "tt_dev_fill_uniform", "tt_launch_count", "tt_build_info",
+    "tt_dev_gemm", "tt_dev_fill_uniform", "tt_launch_count", "tt_build_info", "tt_dag_tasks",
 )
 
 _lib = None
@@ -69,6 +69,7 @@ def load() -> ctypes.CDLL:
                                         ctypes.c_uint64, c_int, vp]),
         "tt_launch_count": (ctypes.c_uint64, [vp]),
         "tt_build_info": (ctypes.c_char_p, []),
+        "tt_dag_tasks": (c_int, [c_int, c_int, c_int, c_int, c_int_p, c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -87,3 +88,16 @@ def ptr(a: np.ndarray | None):
 def int_array(values) -> ctypes.Array:
     vals = [int(v) for v in values]
     return (ctypes.c_int * max(len(vals), 1))(*vals)
+
+
+def dag_tasks(kernel: str, n: int, by: int, bx: int) -> np.ndarray | None:
+    """Task list of the persistent tile-DAG schedule as an (ntasks, 4) int array
+    {kind | j << 2, k, r0, r1}, or None when (n, by, bx) uses the graph schedule."""
+    lib = load()
+    kid = KERNEL_IDS[kernel]
+    cnt = lib.tt_dag_tasks(kid, n, by, bx, None, 0)
+    if cnt < 0:
+        return None
+    out = np.zeros((cnt, 4), dtype=np.int32)
+    lib.tt_dag_tasks(kid, n, by, bx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), cnt)
+    return out

@@ -1,0 +1,66 @@
+// Persistent tile-DAG schedule for LU (no pivoting) and Cholesky (sm_100a).
+//
+// The graph schedule (schedules.cu) issues ~4 dependent launches per panel
+// step, so at PolyBench sizes the factorisation is bound by launch and
+// panel latency.  This schedule runs the WHOLE factorisation as
+// one launch: one CTA per SM pulls tasks from a host-built, priority-ordered
+// task list and waits on per-tile completion counters in L2, so the next
+// panel's diagonal block is factored while the current trailing update is
+// still running (look-ahead), with no kernel boundaries on the critical path.
+//
+// Tiles are bx x bx (the reference's panel width, kernels.cpp:181-182); the
+// trailing-update and panel-solve tasks cover row regions of `by` rows
+// anchored at the panel end, exactly the reference's trailing tiling
+// (kernels.cpp:205-216).  Task kinds, per panel step k:
+//   DIAG(k)           getrf / potrf of tile (k,k) in shared memory
+//   TRSM_L(k, rows)   L21 = A21 U11^-1 (LU) / A21 L11^-T (Cholesky)
+//   TRSM_U(k, j)      U12 = L11^-1 A12 (LU only)
+//   GEMM(k, rows, j)  A(rows, j) -= L(rows, k) * U(k, j)   (Cholesky: L(j,k)^T)
+// GEMM and TRSM run on the fp64 tensor cores (DMMA m8n8k4); the triangular
+// solves are blocked by 8 columns with 8x8 diagonal-block inverses.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <vector>
+
+namespace tt {
+namespace dag {
+
+enum TaskKind : int { kDiag = 0, kTrsmL = 1, kTrsmU = 2, kGemm = 3 };
+
+// Widest tile the persistent kernel handles (the diag block is factored by
+// the warp-register code of diag_factor.cuh, <= 64).
+constexpr int kMaxTile = 64;
+constexpr int kMinTile = 8;
+constexpr long long kMaxTasks = 8LL << 20;
+
+// Watchdog: a dependency wait longer than this aborts the schedule with
+// info = kTimeout (a scheduling bug must never hang the GPU).
+constexpr long long kWatchdogNs = 4000000000LL;
+constexpr int kTimeout = -2147483647 - 1;  // INT_MIN
+
+// True when the persistent schedule covers (n, by, bx).
+bool eligible(int n, int by, int bx);
+
+// Host-built task list in dependency-respecting priority order
+// (int4 {kind | j << 2, k, r0, r1}).
+std::vector<int4> build_tasks(bool chol, int n, int by, int bx);
+
+struct Workspace {
+  int4* tasks = nullptr;   // device task list
+  int ntasks = 0;
+  int* cnt = nullptr;      // nt*nt tile counters + 1 task counter + 1 abort flag
+  size_t cnt_bytes = 0;
+  int grid = 0;
+};
+
+// Allocates and uploads the workspace for one (kernel, n, by, bx, buffer).
+cudaError_t create(Workspace* w, bool chol, int n, int by, int bx);
+void destroy(Workspace* w);
+
+// Enqueues counter reset + the persistent kernel on `s` (graph-capturable).
+cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long ld, int bx,
+                    int* info, cudaStream_t s);
+
+}  // namespace dag
+}  // namespace tt

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/tt_gpu.h"
+#include "dag_factor.cuh"
 #include "factor_kernels.cuh"
 #include "gemm.hpp"
 #include "schedules.cuh"
@@ -71,6 +72,7 @@ struct tt_ctx {
   tt::TmapCache tmaps;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GraphKey, long long> graph_nodes;
+  std::map<GraphKey, tt::dag::Workspace> dag_ws;  // persistent-schedule task lists + counters
   unsigned long long launches = 0;
   bool have_output = false;
 };
@@ -236,18 +238,39 @@ int get_graph(tt_ctx* ctx, const GraphKey& key, Enqueue&& enq, cudaGraphExec_t* 
   return TT_OK;
 }
 
+// Factorisation schedule: TT_FACTOR_SCHEDULE=graph forces the launch-per-kernel
+// graph (schedules.cu); otherwise the persistent tile-DAG kernel
+// (dag_factor.cu) runs whenever it covers (n, by, bx).
+bool use_dag_schedule(int n, int by, int bx) {
+  static const bool graph_only = [] {
+    const char* v = std::getenv("TT_FACTOR_SCHEDULE");
+    return v && std::strcmp(v, "graph") == 0;
+  }();
+  return !graph_only && tt::dag::eligible(n, by, bx);
+}
+
 int factor_graph(tt_ctx* ctx, int kernel, double* a, int n, long long ld, int by, int bx,
                  cudaGraphExec_t* g, long long* nodes) {
-  GraphKey key{kernel == TT_KERNEL_LU ? kGraphLu : kGraphChol,
-               {reinterpret_cast<long long>(a), n, ld, by, bx}};
+  const bool chol = kernel != TT_KERNEL_LU;
+  const bool dag = use_dag_schedule(n, by, bx);
+  GraphKey key{chol ? kGraphChol : kGraphLu,
+               {reinterpret_cast<long long>(a), n, ld, by, bx, dag ? 1 : 0}};
+  tt::dag::Workspace* w = nullptr;
+  if (dag) {  // allocated outside stream capture
+    w = &ctx->dag_ws[key];
+    if (!w->tasks) TT_CUDA(ctx, tt::dag::create(w, chol, n, by, bx), "dag workspace");
+  }
   return get_graph(
       ctx, key,
       [&](tt::ScheduleStats* st) {
+        if (dag) {
+          st->launches += 1;
+          return tt::dag::enqueue(*w, chol, a, n, ld, bx, ctx->info, ctx->stream);
+        }
         const tt::Streams ss{ctx->stream, ctx->stream2, ctx->fork, ctx->join};
-        return kernel == TT_KERNEL_LU
-                   ? tt::enqueue_lu(ctx->tmaps, a, n, ld, by, bx, ctx->ws, ctx->info, ss, st)
-                   : tt::enqueue_cholesky(ctx->tmaps, a, n, ld, by, bx, ctx->ws, ctx->info, ss,
-                                          st);
+        return !chol ? tt::enqueue_lu(ctx->tmaps, a, n, ld, by, bx, ctx->ws, ctx->info, ss, st)
+                     : tt::enqueue_cholesky(ctx->tmaps, a, n, ld, by, bx, ctx->ws, ctx->info, ss,
+                                            st);
       },
       g, nodes);
 }
@@ -327,6 +350,8 @@ int enqueue_run(tt_ctx* ctx, const int* cfg, cudaEvent_t ev_start, cudaEvent_t e
 
 int numeric_status(tt_ctx* ctx, int info, int* fail_index) {
   if (info == tt::kNoFailure) return TT_OK;
+  if (info == tt::dag::kTimeout)
+    return fail(ctx, TT_EDEVICE, "persistent schedule watchdog: dependency wait timed out");
   if (fail_index) *fail_index = info;
   if (ctx->kernel == TT_KERNEL_CHOLESKY)
     return fail(ctx, TT_ENUMERIC, "cholesky: non-positive diagonal at row %d", info);
@@ -424,6 +449,7 @@ int tt_ctx_destroy(tt_ctx* ctx) {
   if (!ctx) return TT_OK;
   cudaSetDevice(ctx->device);
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : ctx->dag_ws) tt::dag::destroy(&kv.second);
   for (auto* m : {&ctx->work, &ctx->e, &ctx->f, &ctx->g, &ctx->scratch_l, &ctx->scratch_u,
                   &ctx->oneshot})
     release(*m);
@@ -827,6 +853,21 @@ int tt_dev_fill_uniform(tt_ctx* ctx, double* a, int rows, int cols, int ld, long
   TT_CUDA(ctx, cudaGetLastError(), "fill_uniform");
   ctx->launches += 1;
   return TT_OK;
+}
+
+int tt_dag_tasks(int kernel, int n, int by, int bx, int* out, int cap) {
+  if (!tt::dag::eligible(n, by, bx)) return -1;
+  const std::vector<int4> v = tt::dag::build_tasks(kernel != TT_KERNEL_LU, n, by, bx);
+  if (out) {
+    const size_t m = std::min(v.size(), static_cast<size_t>(std::max(cap, 0)));
+    for (size_t i = 0; i < m; ++i) {
+      out[4 * i] = v[i].x;
+      out[4 * i + 1] = v[i].y;
+      out[4 * i + 2] = v[i].z;
+      out[4 * i + 3] = v[i].w;
+    }
+  }
+  return static_cast<int>(v.size());
 }
 
 int tt_dev_gemm(tt_ctx* ctx, const double* a, int lda, const double* b, int ldb, int b_trans,
