@@ -17,6 +17,7 @@
 // which CTA runs a task or when: repeated runs are bitwise identical
 // (kernels_test.cpp:284-296).
 #include <climits>
+#include <cstdlib>
 
 #include "dag_factor.cuh"
 #include "diag_factor.cuh"
@@ -36,6 +37,25 @@ constexpr int kStrip = 8 * kMF;   // rows per warp strip
 // pair exactly twice — the 2-wavefront minimum for 256 bytes.
 constexpr int kNP = 68;
 constexpr int kNoLower = INT_MAX / 2;
+// Per-warp double-buffered A strips (16 rows x <= 66 columns, row stride
+// kAW == 4 mod 16: conflict-free A-fragment loads) staged by cp.async.cg.
+constexpr int kAW = 68;
+constexpr int kABuf = kStrip * kAW;              // doubles per buffer
+constexpr int kSmemB = kIB * kNP;                // B / M tile
+constexpr int kSmemA = kWarps * 2 * kABuf;       // all warps' A buffers
+constexpr int kSmemBytes = (kSmemB + kSmemA + 8 * 64 + 2 * 132 + 128) * 8;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 struct Params {
   double* a;
@@ -47,13 +67,9 @@ struct Params {
   int* next;   // task counter
   int* abort;  // 1: numerical failure, 2: watchdog
   int* info;
+  unsigned long long* trace;  // optional: per task {fetch, ready, done ns, smid, 4 phase stamps}
 };
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -65,43 +81,104 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Thread 0 only.  False when the schedule was aborted.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Spins (relaxed gpu-scope loads: no L1 invalidation per poll, with a short
+// back-off so waiting CTAs do not hammer the counter's L2 slice) until
+// *addr >= need, then one acquire fence.  False when the schedule was aborted.
 __device__ bool wait_ge(const Params& p, const int* addr, int need) {
-  if (ld_acquire(addr) >= need) return true;
-  const unsigned long long t0 = globaltimer();
-  for (;;) {
-    if (ld_acquire(addr) >= need) return true;
-    if (*reinterpret_cast<volatile int*>(p.abort)) return false;
-    if (globaltimer() - t0 > static_cast<unsigned long long>(kWatchdogNs)) {
-      atomicExch(p.abort, 2);
-      atomicMin(p.info, kTimeout);
-      return false;
+  if (ld_relaxed(addr) < need) {
+    const unsigned long long t0 = globaltimer();
+    for (int it = 0;; ++it) {
+      __nanosleep(100);
+      if (ld_relaxed(addr) >= need) break;
+      if ((it & 15) == 15) {
+        if (ld_relaxed(p.abort)) return false;
+        if (globaltimer() - t0 > static_cast<unsigned long long>(kWatchdogNs)) {
+          atomicExch(p.abort, 2);
+          atomicMin(p.info, kTimeout);
+          return false;
+        }
+      }
     }
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  return true;
+}
+
+// Task-level dependencies: what the whole CTA reads (the diagonal tile, the
+// B operand).  Row-strip dependencies (the strip's own output tiles and its
+// L rows) are waited for per strip by the warp that processes it, so a
+// task's first strips start as soon as their rows are ready (dataflow along
+// the rows: DIAG(k) -> first TRSM_L strips -> first GEMM strips -> DIAG(k+1)).
+template <bool CHOL>
+__device__ __forceinline__ int dep_count(int kind) {
+  return kind == kTrsmU ? 2 : 1;
+}
+
+template <bool CHOL>
+__device__ __forceinline__ void dep_at(const Params& p, int kind, int j, int k, int d, int* idx,
+                                       int* need) {
+  const int T = p.T, nt = p.nt, kT = k * T;
+  switch (kind) {
+    case kDiag:  // stage k-1 of tile (k,k)
+      *idx = k * nt + k;
+      *need = kT;
+      return;
+    case kTrsmL:  // DIAG(k)
+      *idx = k * nt + k;
+      *need = kT + T;
+      return;
+    case kTrsmU:  // stage k-1 of tile (k,j), DIAG(k)
+      *idx = d == 0 ? k * nt + j : k * nt + k;
+      *need = d == 0 ? kT : kT + T;
+      return;
+    default:  // kGemm: B operand U(k, j) / L(j, k) final
+      *idx = CHOL ? j * nt + k : k * nt + j;
+      *need = kT + T;
   }
 }
 
 template <bool CHOL>
 __device__ bool wait_deps(const Params& p, int4 tk) {
-  const int kind = tk.x & 3, j = tk.x >> 2, k = tk.y, r0 = tk.z, r1 = tk.w;
-  const int T = p.T, nt = p.nt, kT = k * T;
-  const int* cnt = p.cnt;
-  switch (kind) {
-    case kDiag:  // stage k-1 of tile (k,k)
-      return wait_ge(p, &cnt[k * nt + k], kT);
-    case kTrsmL:  // stage k-1 of the row tiles, then DIAG(k)
-      for (int i = r0 / T; i * T < r1; ++i)
-        if (!wait_ge(p, &cnt[i * nt + k], kT)) return false;
-      return wait_ge(p, &cnt[k * nt + k], kT + T);
-    case kTrsmU:
-      if (!wait_ge(p, &cnt[k * nt + j], kT)) return false;
-      return wait_ge(p, &cnt[k * nt + k], kT + T);
-    default:  // kGemm: stage k-1 of the output tiles, L(rows, k) and U(k, j) / L(j, k) final
-      for (int i = r0 / T; i * T < r1; ++i) {
-        if (!wait_ge(p, &cnt[i * nt + j], kT)) return false;
-        if (!wait_ge(p, &cnt[i * nt + k], kT + T)) return false;
-      }
-      return wait_ge(p, CHOL ? &cnt[j * nt + k] : &cnt[k * nt + j], kT + T);
+  const int kind = tk.x & 3, j = tk.x >> 2, k = tk.y;
+  const int nd = dep_count<CHOL>(kind);
+  bool ok = true;
+  const int d = threadIdx.x & 31;
+  if (d < nd) {
+    int idx, need;
+    dep_at<CHOL>(p, kind, j, k, d, &idx, &need);
+    ok = wait_ge(p, &p.cnt[idx], need);
   }
+  return __all_sync(0xffffffffu, ok);
+}
+
+// Row-strip dependencies of rows [rs, re) writing tile column `col` at step
+// k: stage k-1 of the output tiles, and (GEMM) the L tiles (i, k) final.
+// Lane d of the calling warp takes dependency d.  With `block` false this is
+// a single poll (true only if everything is already satisfied).
+__device__ __forceinline__ bool strip_deps(const Params& p, int rs, int re, int col, int k,
+                                           bool gemm, bool block) {
+  const int T = p.T, nt = p.nt, kT = k * T;
+  const int ti0 = rs / T, nti = (re - 1) / T - ti0 + 1;
+  const int d = threadIdx.x & 31;
+  bool ok = true;
+  if (d < (gemm ? 2 * nti : nti)) {
+    const int i = ti0 + (d < nti ? d : d - nti);
+    const int* c = &p.cnt[i * nt + (d < nti ? col : k)];
+    const int need = d < nti ? kT : kT + T;
+    if (block) {
+      ok = wait_ge(p, c, need);
+    } else {
+      ok = ld_relaxed(c) >= need;
+      if (ok) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+  }
+  return __all_sync(0xffffffffu, ok);
 }
 
 // All lanes of a warp, after storing rows [ra, rb) of tile column j.
@@ -117,59 +194,290 @@ __device__ __forceinline__ void warp_signal(const Params& p, int ra, int rb, int
 }
 
 // ---------------------------------------------------------------- GEMM
-// C[r, c] (r < nrows, c < T) -= sum_k A[r, k] * B[k, c]  with B (Kp x Tp,
-// zero-padded) in shared memory; one warp, 16 rows, DMMA 8x8x4 atoms.
-// Stores only where r + lower_off >= c (Cholesky diagonal tiles).
+// One warp's share of a GEMM task: C[r, c] -= sum_k A[r, k] * B[k, c] over
+// the 16-row strips ra = r0 + 16*warp, +128, ... of rows [r0, r1).  B (Kp x
+// Tp, zero-padded) is in shared memory.  Software pipeline per strip: the
+// next strip's A (cp.async.cg into the warp's other buffer, L2 only) and C
+// (registers) are in flight while this strip's DMMAs run; the strip is
+// published (fence + red.release) right after its stores.  Stores only
+// where row + lower_off >= col (Cholesky diagonal tiles).
 template <int NF>
-__device__ __forceinline__ void warp_gemm(const double* __restrict__ A, long long lda,
-                                          double* __restrict__ C, long long ldc, int nrows, int T,
-                                          const double* __restrict__ Bs, int lower_off) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  double acc[kMF][NF][2];
-  double af[kMF][2 * NF];
-#pragma unroll
-  for (int mf = 0; mf < kMF; ++mf) {
-    const int r = mf * 8 + g;
-    const bool rv = r < nrows;
-    const double* crow = C + static_cast<long long>(rv ? r : 0) * ldc;
-    const double* arow = A + static_cast<long long>(rv ? r : 0) * lda;
-#pragma unroll
-    for (int nf = 0; nf < NF; ++nf)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = nf * 8 + 2 * t + h;
-        acc[mf][nf][h] = (rv && c < T) ? __ldcg(crow + c) : 0.0;
-      }
-#pragma unroll
-    for (int s = 0; s < 2 * NF; ++s) {
-      const int kk = 4 * s + t;
-      af[mf][s] = (rv && kk < T) ? -__ldcg(arow + kk) : 0.0;
+__device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int k, int j,
+                                            const double* __restrict__ Bs, double* abuf,
+                                            bool chol) {
+  const int kT = k * p.T, jT = j * p.T;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
+  const int T = p.T;
+  const long long ld = p.ld;
+  const int col0 = kT & ~1, sh = kT - col0;            // 16-byte aligned copy origin
+  const int nvec = (kT + T - col0 + 1) >> 1;           // 16-byte vectors per row
+  int ra = r0 + warp * kStrip;
+  if (ra >= r1) return;
+
+  auto issue_a = [&](int rs, double* buf) {
+    const int nr = min(kStrip, r1 - rs);
+    const double* src = p.a + static_cast<long long>(rs) * ld + col0;
+    for (int e = lane; e < nr * nvec; e += 32) {
+      const int r = e / nvec, v = e - r * nvec;
+      cp_async16(buf + r * kAW + 2 * v, src + static_cast<long long>(r) * ld + 2 * v);
     }
-  }
+    cp_async_commit();
+  };
+  auto load_c = [&](int rs, double (&cv)[kMF][NF][2]) {
+    const int nr = min(kStrip, r1 - rs);
 #pragma unroll
-  for (int s = 0; s < 2 * NF; ++s) {
-    if (4 * s < T) {
-      double b[NF];
-#pragma unroll
-      for (int nf = 0; nf < NF; ++nf) b[nf] = Bs[(4 * s + t) * kNP + nf * 8 + g];
-#pragma unroll
-      for (int mf = 0; mf < kMF; ++mf)
-#pragma unroll
-        for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], af[mf][s], b[nf]);
-    }
-  }
-#pragma unroll
-  for (int mf = 0; mf < kMF; ++mf) {
-    const int r = mf * 8 + g;
-    if (r < nrows) {
-      double* crow = C + static_cast<long long>(r) * ldc;
+    for (int mf = 0; mf < kMF; ++mf) {
+      const int r = mf * 8 + g;
+      const bool rv = r < nr;
+      const double* crow = p.a + static_cast<long long>(rs + (rv ? r : 0)) * ld + jT;
 #pragma unroll
       for (int nf = 0; nf < NF; ++nf)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = nf * 8 + 2 * t + h;
-          if (c < T && r + lower_off >= c) crow[c] = acc[mf][nf][h];
+          cv[mf][nf][h] = (rv && c < T) ? __ldcg(crow + c) : 0.0;
         }
+    }
+  };
+
+  double acc[kMF][NF][2];
+  if (!strip_deps(p, ra, min(ra + kStrip, r1), j, k, true, true)) return;
+  issue_a(ra, abuf);
+  load_c(ra, acc);
+  int cur = 0;
+  for (;;) {
+    const int rn = ra + kWarps * kStrip;
+    const bool more = rn < r1;
+    double cn[kMF][NF][2];
+    // prefetch the next strip now if its rows are already final, else after this one
+    const bool pref = more && strip_deps(p, rn, min(rn + kStrip, r1), j, k, true, false);
+    if (pref) {
+      issue_a(rn, abuf + (cur ^ 1) * kABuf);
+      load_c(rn, cn);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    const int nr = min(kStrip, r1 - ra);
+    const double* ab = abuf + cur * kABuf + sh;
+#pragma unroll
+    for (int s = 0; s < 2 * NF; ++s) {
+      if (4 * s < T) {
+        const int kk = 4 * s + t;
+        double af[kMF];
+#pragma unroll
+        for (int mf = 0; mf < kMF; ++mf) {
+          const int r = mf * 8 + g;
+          af[mf] = (r < nr && kk < T) ? -ab[r * kAW + kk] : 0.0;
+        }
+        double bf[NF];
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf) bf[nf] = Bs[kk * kNP + nf * 8 + g];
+#pragma unroll
+        for (int mf = 0; mf < kMF; ++mf)
+#pragma unroll
+          for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], af[mf], bf[nf]);
+      }
+    }
+    const int lower_off = chol ? ra - jT : kNoLower;
+#pragma unroll
+    for (int mf = 0; mf < kMF; ++mf) {
+      const int r = mf * 8 + g;
+      if (r < nr) {
+        double* crow = p.a + static_cast<long long>(ra + r) * ld + jT;
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = nf * 8 + 2 * t + h;
+            if (c < T && r + lower_off >= c) crow[c] = acc[mf][nf][h];
+          }
+      }
+    }
+    warp_signal(p, ra, ra + nr, j);
+    if (!more) break;
+    if (!pref) {
+      if (!strip_deps(p, rn, min(rn + kStrip, r1), j, k, true, true)) return;
+      issue_a(rn, abuf + (cur ^ 1) * kABuf);
+      load_c(rn, cn);
+    }
+#pragma unroll
+    for (int mf = 0; mf < kMF; ++mf)
+#pragma unroll
+      for (int nf = 0; nf < NF; ++nf) {
+        acc[mf][nf][0] = cn[mf][nf][0];
+        acc[mf][nf][1] = cn[mf][nf][1];
+      }
+    ra = rn;
+    cur ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------- DIAG
+// Reciprocal: MUFU seed + two Newton steps (~50 cycles vs ~110 for the IEEE
+// division sequence) — the pivot reciprocal sits on the factorisation's
+// serial chain.  Within 1 ulp of 1/x for the normal pivots that pass the
+// reference's failure checks.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+constexpr int kPB = 132;  // doubles per parity of the DIAG publication buffer
+
+// getrf / potrf of one T x T tile (T <= 64) by 8 warps, register resident:
+// warp w owns rows 8w..8w+7, lane l owns columns l and l+32.  Step k needs
+// the final pivot row k (LU), column k and the reciprocal of the pivot,
+// which their owners publish in shared memory at the end of step k-1
+// (double-buffered by step parity; one __syncthreads per pivot).  Warps
+// whose rows are all finished skip the step; T <= 32 skips the upper column
+// half.  The step is branch- and select-free for all but the warp holding
+// row k: columns <= k see a zero operand (x - m*0 = x), and the multipliers
+// l_ik = a_ik * (1/a_kk) are formed once at the end from the per-column
+// reciprocals (column k is never touched after step k).  Per element the
+// reference panel's operation order (kernels.cpp:186-196 / :289-306); the
+// reciprocal-multiply is <= 1 ulp from the reference's division.
+template <bool CHOL>
+__device__ __forceinline__ void tile_factor(double* __restrict__ dk, long long ld, int T, int gcol,
+                                            int* info, double* pbuf, double* rk,
+                                            unsigned long long* ph) {
+  // pbuf parity block: [0,64) pivot row (LU), [64,128) column k, [128] 1/pivot, [129] l_kk
+  // rk[c]: 1/pivot of column c (LU) or 1/l_cc (Cholesky); rk[64 + c]: l_cc
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i0 = 8 * w;
+  const bool wide = T > 32;
+  double x[8][2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int i = i0 + q;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      x[q][h] = (i < T && c < T && (!CHOL || c <= i))
+                    ? __ldcg(dk + static_cast<long long>(i) * ld + c) : 0.0;
+    }
+  }
+  // publish step 0: column 0 (+ row 0 for LU) and the pivot's reciprocal
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pbuf[64 + i0 + q] = x[q][0];
+  }
+  if (w == 0) {
+    if (!CHOL) {
+      pbuf[lane] = x[0][0];
+      pbuf[lane + 32] = x[0][1];
+    }
+    if (lane == 0) {
+      const double d = x[0][0];
+      if (!CHOL) {
+        if (fabs(d) < 1e-300) atomicMin(info, gcol);  // kernels.cpp:187-190
+        rk[0] = pbuf[128] = rcp_nr(d);
+      } else {
+        if (d <= 0.0) atomicMin(info, gcol);  // kernels.cpp:297-302 (NaN passes)
+        const double l0 = sqrt(d);
+        rk[64] = pbuf[129] = l0;
+        rk[0] = pbuf[128] = rcp_nr(l0);
+      }
+    }
+  }
+  __syncthreads();
+  if (ph && threadIdx.x == 0) ph[0] = globaltimer();
+  for (int k = 0; k < T; ++k) {
+    const double* cb = pbuf + (k & 1) * kPB;
+    double* nb = pbuf + ((k + 1) & 1) * kPB;
+    const int k1 = k + 1;
+    if (i0 + 7 > k) {  // warp-uniform: this warp still has rows > k
+      const double r = cb[128];
+      double m[8];
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(cb + 64 + i0 + q);
+        m[q] = v.x * r;
+        m[q + 1] = v.y * r;
+      }
+      if (i0 <= k) {  // the warp holding row k: rows <= k are final
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (i0 + q <= k) m[q] = 0.0;
+      }
+      // operand row: LU pivot row k, Cholesky l_ck = a_ck / l_kk; 0 for columns <= k
+      const double* src = CHOL ? cb + 64 : cb;
+      const double sc = CHOL ? r : 1.0;
+      const double u0 = lane > k ? src[lane] * sc : 0.0;
+      if (wide) {
+        const double u1 = lane + 32 > k ? src[lane + 32] * sc : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          x[q][0] = fma(-m[q], u0, x[q][0]);
+          x[q][1] = fma(-m[q], u1, x[q][1]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q][0] = fma(-m[q], u0, x[q][0]);
+      }
+      if (k1 < T) {
+        // publish column k+1 of my rows (the lane holding it)
+        if (lane == (k1 & 31)) {
+          if (k1 >= 32) {
+#pragma unroll
+            for (int q = 0; q < 8; q += 2)
+              *reinterpret_cast<double2*>(nb + 64 + i0 + q) = make_double2(x[q][1], x[q + 1][1]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; q += 2)
+              *reinterpret_cast<double2*>(nb + 64 + i0 + q) = make_double2(x[q][0], x[q + 1][0]);
+          }
+        }
+        // publish row k+1 (LU) and the next pivot's reciprocal (its owner warp)
+        if ((k1 >> 3) == w) {
+          const int q1 = k1 & 7;
+          double v0 = x[0][0], v1 = x[0][1];
+#pragma unroll
+          for (int q = 1; q < 8; ++q)
+            if (q == q1) {
+              v0 = x[q][0];
+              v1 = x[q][1];
+            }
+          if (!CHOL) {
+            nb[lane] = v0;
+            nb[lane + 32] = v1;
+          }
+          if (lane == (k1 & 31)) {
+            const double d = k1 >= 32 ? v1 : v0;
+            if (!CHOL) {
+              if (fabs(d) < 1e-300) atomicMin(info, gcol + k1);  // kernels.cpp:187-190
+              rk[k1] = nb[128] = rcp_nr(d);
+            } else {
+              if (d <= 0.0) atomicMin(info, gcol + k1);  // kernels.cpp:297-302
+              const double l1 = sqrt(d);
+              rk[64 + k1] = nb[129] = l1;
+              rk[k1] = nb[128] = rcp_nr(l1);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (ph && threadIdx.x == 0) ph[1] = globaltimer();
+  // multipliers below the diagonal (and l_cc on it for Cholesky), then store
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int i = i0 + q;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (i < T && c < T && (!CHOL || c <= i)) {
+        double v = x[q][h];
+        if (c < i) v *= rk[c];
+        if (CHOL && c == i) v = rk[64 + c];
+        dk[static_cast<long long>(i) * ld + c] = v;
+      }
     }
   }
 }
@@ -316,45 +624,62 @@ __device__ __forceinline__ void load_m(double* Ms, const double* __restrict__ d,
 template <int NF, bool CHOL>
 __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
   constexpr int Tp = NF * 8;
-  __shared__ __align__(16) double sm[kIB * diag::kLd > Tp * kNP ? kIB * diag::kLd : Tp * kNP];
-  __shared__ __align__(16) double minv[8 * 64];
-  __shared__ __align__(16) double buf[64];
-  __shared__ int4 s_task;
+  extern __shared__ __align__(16) double dsm[];
+  double* sm = dsm;                      // B (GEMM) / M (TRSM): Tp x kNP
+  double* abuf = dsm + kSmemB;           // per-warp A strips
+  double* minv = abuf + kSmemA;          // 8 x (8x8) block inverses
+  double* pbuf = minv + 8 * 64;          // DIAG: 2 x kPB
+  double* rk = pbuf + 2 * kPB;           // DIAG: 128 per-column reciprocals / l_cc
+  __shared__ int4 s_task[2];
+  __shared__ int s_id[2];
   __shared__ int s_go;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  __shared__ unsigned long long s_t0, s_t1, s_ph[4];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = p.T, nt = p.nt;
+  auto stamp = [&](int i) {
+    if (p.trace && tid == 0) s_ph[i] = globaltimer();
+  };
   const long long ld = p.ld;
+  const int4 kNone = make_int4(-1, 0, 0, 0);
 
-  for (;;) {
-    if (tid == 0) {
-      const int id = atomicAdd(p.next, 1);
-      int4 tk = make_int4(-1, 0, 0, 0);
-      if (id < p.ntasks) tk = p.tasks[id];
-      s_task = tk;
-      s_go = tk.x >= 0 && wait_deps<CHOL>(p, tk);
+  if (tid == 0) {
+    const int id = atomicAdd(p.next, 1);
+    s_id[0] = id;
+    s_task[0] = id < p.ntasks ? p.tasks[id] : kNone;
+  }
+  __syncthreads();
+  for (int it = 0;; ++it) {
+    const int cur = it & 1;
+    const int4 tk = s_task[cur];
+    if (warp == 0) {
+      // prefetch the next task index; its latency overlaps the dependency wait
+      int nid = 0;
+      if (lane == 0) {
+        if (p.trace) s_t0 = globaltimer();
+        if (tk.x >= 0) nid = atomicAdd(p.next, 1);
+      }
+      const bool ok = tk.x >= 0 && wait_deps<CHOL>(p, tk);
+      if (lane == 0) {
+        __threadfence();
+        s_go = ok;
+        s_id[cur ^ 1] = nid;
+        s_task[cur ^ 1] = (tk.x >= 0 && nid < p.ntasks) ? p.tasks[nid] : kNone;
+        if (p.trace) {
+          s_t1 = globaltimer();
+          s_ph[2] = clock64();
+        }
+      }
     }
     __syncthreads();
     if (!s_go) break;
-    const int4 tk = s_task;
     const int kind = tk.x & 3, j = tk.x >> 2, k = tk.y, r0 = tk.z, r1 = tk.w;
     const int kT = k * T;
     double* dk = p.a + static_cast<long long>(kT) * ld + kT;  // diagonal tile (k,k)
 
+    stamp(0);
+    stamp(1);
     if (kind == kDiag) {
-      double(*D)[diag::kLd] = reinterpret_cast<double(*)[diag::kLd]>(sm);
-      for (int e = tid; e < T * T; e += kThreads) {
-        const int i = e / T, c = e - i * T;
-        D[i][c] = (!CHOL || c <= i) ? __ldcg(dk + static_cast<long long>(i) * ld + c) : 0.0;
-      }
-      __syncthreads();
-      if (CHOL)
-        diag::block_potrf(D, buf, T, kT, p.info, true);  // diag <= 0 fails, kernels.cpp:297-302
-      else
-        diag::block_getrf(D, buf, T, kT, p.info, true);  // |pivot| < 1e-300, kernels.cpp:187-190
-      for (int e = tid; e < T * T; e += kThreads) {
-        const int i = e / T, c = e - i * T;
-        if (!CHOL || c <= i) dk[static_cast<long long>(i) * ld + c] = D[i][c];
-      }
+      tile_factor<CHOL>(dk, ld, T, kT, p.info, pbuf, rk, p.trace ? s_ph : nullptr);
       __threadfence();
       __syncthreads();
       if (tid == 0) {
@@ -376,13 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
           sm[x * kNP + y] = v;
       }
       __syncthreads();
-      const int jT = j * T;
-      for (int ra = r0 + warp * kStrip; ra < r1; ra += kWarps * kStrip) {
-        const int nr = min(kStrip, r1 - ra);
-        double* rowp = p.a + static_cast<long long>(ra) * ld;
-        warp_gemm<NF>(rowp + kT, ld, rowp + jT, ld, nr, T, sm, CHOL ? ra - jT : kNoLower);
-        warp_signal(p, ra, ra + nr, j);
-      }
+      gemm_strips<NF>(p, r0, r1, k, j, sm, abuf + warp * 2 * kABuf, CHOL);
     } else {  // TRSM
       const bool lsolve = kind == kTrsmL;
       load_m(sm, dk, ld, T, Tp, !CHOL && lsolve, !CHOL && !lsolve);
@@ -392,6 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
       if (lsolve) {
         for (int ra = r0 + warp * kStrip; ra < r1; ra += kWarps * kStrip) {
           const int nr = min(kStrip, r1 - ra);
+          if (!strip_deps(p, ra, ra + nr, k, k, false, true)) break;
           warp_trsm<NF>(p.a + static_cast<long long>(ra) * ld + kT, ld, 1, nr, T, sm, minv);
           warp_signal(p, ra, ra + nr, k);
         }
@@ -401,17 +721,39 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
           warp_trsm<NF>(dk + static_cast<long long>(j - k) * T + c0, 1, ld, nc, T, sm, minv);
           __threadfence();
           __syncwarp();
-          if ((tid & 31) == 0) red_release_add(&p.cnt[k * nt + j], nc);
+          if (lane == 0) red_release_add(&p.cnt[k * nt + j], nc);
         }
       }
     }
-    __syncthreads();  // shared tiles are reused by the next task
+    __syncthreads();  // shared tiles and the task slot are reused next iteration
+    if (p.trace && tid == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      unsigned long long* tr = p.trace + 8 * static_cast<long long>(s_id[cur]);
+      tr[0] = s_t0;
+      tr[1] = s_t1;
+      tr[2] = globaltimer();
+      tr[3] = smid;
+      s_ph[3] = clock64();
+      tr[4] = s_ph[0];
+      tr[5] = s_ph[1];
+      tr[6] = s_ph[2];
+      tr[7] = s_ph[3];
+    }
   }
 }
 
 template <int NF, bool CHOL>
 cudaError_t launch(const Params& prm, int grid, cudaStream_t s) {
-  dag_kernel<NF, CHOL><<<grid, kThreads, 0, s>>>(prm);
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e = cudaFuncSetAttribute(dag_kernel<NF, CHOL>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               kSmemBytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dag_kernel<NF, CHOL><<<grid, kThreads, kSmemBytes, s>>>(prm);
   return cudaGetLastError();
 }
 
@@ -492,6 +834,11 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   if (e != cudaSuccess) return e;
   e = cudaMalloc(&w->cnt, w->cnt_bytes);
   if (e != cudaSuccess) return e;
+  const char* tr = std::getenv("TT_DAG_TRACE");
+  if (tr && tr[0] == '1') {
+    e = cudaMalloc(&w->trace, tasks.size() * 8 * sizeof(unsigned long long));
+    if (e != cudaSuccess) return e;
+  }
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -502,6 +849,7 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
 void destroy(Workspace* w) {
   if (w->tasks) cudaFree(w->tasks);
   if (w->cnt) cudaFree(w->cnt);
+  if (w->trace) cudaFree(w->trace);
   *w = Workspace{};
 }
 
@@ -522,6 +870,7 @@ cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long l
   prm.next = w.cnt + static_cast<size_t>(nt) * nt;
   prm.abort = prm.next + 1;
   prm.info = info;
+  prm.trace = w.trace;
   const int nf = (bx + 7) / 8;
   return chol ? launch_nf<true>(nf, prm, w.grid, s) : launch_nf<false>(nf, prm, w.grid, s);
 }

@@ -52,6 +52,7 @@ struct Workspace {
   int* cnt = nullptr;      // nt*nt tile counters + 1 task counter + 1 abort flag
   size_t cnt_bytes = 0;
   int grid = 0;
+  unsigned long long* trace = nullptr;  // TT_DAG_TRACE=1: per-task timestamps
 };
 
 // Allocates and uploads the workspace for one (kernel, n, by, bx, buffer).

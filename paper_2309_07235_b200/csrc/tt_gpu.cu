@@ -73,6 +73,7 @@ struct tt_ctx {
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GraphKey, long long> graph_nodes;
   std::map<GraphKey, tt::dag::Workspace> dag_ws;  // persistent-schedule task lists + counters
+  const tt::dag::Workspace* dag_last = nullptr;    // most recently enqueued (for tt_dag_trace)
   unsigned long long launches = 0;
   bool have_output = false;
 };
@@ -259,11 +260,13 @@ int factor_graph(tt_ctx* ctx, int kernel, double* a, int n, long long ld, int by
   if (dag) {  // allocated outside stream capture
     w = &ctx->dag_ws[key];
     if (!w->tasks) TT_CUDA(ctx, tt::dag::create(w, chol, n, by, bx), "dag workspace");
+    ctx->dag_last = w;
   }
   return get_graph(
       ctx, key,
       [&](tt::ScheduleStats* st) {
         if (dag) {
+          ctx->dag_last = w;
           st->launches += 1;
           return tt::dag::enqueue(*w, chol, a, n, ld, bx, ctx->info, ctx->stream);
         }
@@ -868,6 +871,18 @@ int tt_dag_tasks(int kernel, int n, int by, int bx, int* out, int cap) {
     }
   }
   return static_cast<int>(v.size());
+}
+
+int tt_dag_trace(tt_ctx* ctx, unsigned long long* out, int cap) {
+  if (!ctx || !ctx->dag_last || !ctx->dag_last->trace) return -1;
+  const tt::dag::Workspace* w = ctx->dag_last;
+  TT_CUDA(ctx, cudaStreamSynchronize(ctx->stream), "trace sync");
+  const int m = std::min(w->ntasks, std::max(cap, 0));
+  if (out && m > 0)
+    TT_CUDA(ctx, cudaMemcpy(out, w->trace, static_cast<size_t>(m) * 8 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost),
+            "trace copy");
+  return w->ntasks;
 }
 
 int tt_dev_gemm(tt_ctx* ctx, const double* a, int lda, const double* b, int ldb, int b_trans,

@@ -1,0 +1,59 @@
+#!/usr/bin/env python3
+"""Per-task timeline of the persistent tile-DAG schedule (TT_DAG_TRACE=1).
+
+Usage: TT_DAG_TRACE=1 python tools/dag_trace.py lu 2000 400 50 [out.npz]
+Prints per-kind run/wait times and the DIAG critical-chain timeline."""
+import ctypes
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+os.environ["TT_DAG_TRACE"] = "1"
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2309_07235_b200 import Context, GpuKernelRunner, KernelCase, _lib  # noqa: E402
+
+kern, n, by, bx = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+ctx = Context(0)
+r = GpuKernelRunner(KernelCase(kern, n, seed=1), ctx)
+for _ in range(3):
+    r.run((by, bx), want_output=False)
+tasks = _lib.dag_tasks(kern, n, by, bx)
+nt = len(tasks)
+tr = np.zeros((nt, 8), dtype=np.uint64)
+got = ctx.lib.tt_dag_trace(ctx.handle, tr.ctypes.data_as(ctypes.c_void_p), nt)
+assert got == nt, got
+t = tr[:, :3].astype(np.int64)
+t0 = t[:, 0].min()
+t = (t - t0) / 1e3  # us
+kind = tasks[:, 0] & 3
+names = ["DIAG", "TRSM_L", "TRSM_U", "GEMM"]
+span = t[:, 2].max()
+print(f"{kern} n={n} ({by},{bx}): {nt} tasks, span {span:.1f} us, SMs used {len(set(tr[:, 3]))}")
+for k in range(4):
+    m = kind == k
+    if m.any():
+        run = t[m, 2] - t[m, 1]
+        wait = t[m, 1] - t[m, 0]
+        print(f"  {names[k]:6s} n={m.sum():6d} run mean {run.mean():7.2f} max {run.max():7.2f} "
+              f"| wait mean {wait.mean():7.2f} max {wait.max():7.2f} us | busy sum {run.sum():9.1f}")
+dm = kind == 0
+ph = (tr[dm, 4:6].astype(np.int64) - t0) / 1e3
+print("  DIAG phases (us after ready): load+sync %.2f, loop %.2f, rest %.2f" % (
+    (ph[:, 0] - t[dm, 1]).mean(), (ph[:, 1] - ph[:, 0]).mean(), (t[dm, 2] - ph[:, 1]).mean()))
+cyc = tr[:, 7].astype(np.int64) - tr[:, 6].astype(np.int64)
+ns = tr[:, 2].astype(np.int64) - tr[:, 1].astype(np.int64)
+ok = ns > 2000
+print("  effective SM clock during tasks: %.3f GHz (median)" % np.median(cyc[ok] / ns[ok]))
+busy = (t[:, 2] - t[:, 1]).sum()
+grid = len(set(tr[:, 3]))
+print(f"  utilisation (task run time / (SMs x span)) = {busy / (grid * span):.3f}")
+d = np.where(kind == 0)[0]
+print("  DIAG chain (k: ready, done, gap since previous DIAG done):")
+prev = 0.0
+for i, idx in enumerate(d[:8].tolist() + d[-3:].tolist()):
+    print(f"    k={tasks[idx, 1]:4d} ready {t[idx, 1]:8.1f} done {t[idx, 2]:8.1f} gap {t[idx, 1] - prev:7.1f}")
+    prev = t[idx, 2]
+if len(sys.argv) > 5:
+    np.savez(sys.argv[5], tasks=tasks, trace=tr)

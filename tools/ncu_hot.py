@@ -4,6 +4,9 @@ import csv
 import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
+# keep the first kernel section only (a CSV may hold several)
+ends = [i for i, r in enumerate(rows) if i > 0 and r and r[0] == "Kernel Name"]
+rows = rows[:ends[0]] if ends else rows
 hdr = rows[1]
 si = hdr.index("Warp Stall Sampling (All Samples)")
 stall_cols = [i for i, h in enumerate(hdr) if h.startswith("stall_")]
