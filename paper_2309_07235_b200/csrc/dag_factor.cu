@@ -43,7 +43,8 @@ constexpr int kAW = 68;
 constexpr int kABuf = kStrip * kAW;              // doubles per buffer
 constexpr int kSmemB = kIB * kNP;                // B / M tile
 constexpr int kSmemA = kWarps * 2 * kABuf;       // all warps' A buffers
-constexpr int kSmemBytes = (kSmemB + kSmemA + 8 * 64 + 2 * 132 + 128) * 8;
+constexpr int kSmemBytes = (kSmemB + kSmemA + 9 * 64 + 2 * 132 + 128) * 8;
+constexpr int kSolveSlot = 64;  // per step: diagonal reciprocals written by DIAG
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
@@ -68,6 +69,7 @@ struct Params {
   int* abort;  // 1: numerical failure, 2: watchdog
   int* info;
   unsigned long long* trace;  // optional: per task {fetch, ready, done ns, smid, 4 phase stamps}
+  double* solve;  // per step: 64 reciprocals of the factored diagonal (DIAG -> TRSM)
 };
 
 
@@ -204,7 +206,7 @@ __device__ __forceinline__ void warp_signal(const Params& p, int ra, int rb, int
 template <int NF>
 __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int k, int j,
                                             const double* __restrict__ Bs, double* abuf,
-                                            bool chol) {
+                                            bool chol, unsigned long long* first_done) {
   const int kT = k * p.T, jT = j * p.T;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
   const int T = p.T;
@@ -259,6 +261,7 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
       cp_async_wait<0>();
     }
     __syncwarp();
+    if (first_done && lane == 0) first_done[1] = globaltimer();
     const int nr = min(kStrip, r1 - ra);
     const double* ab = abuf + cur * kABuf + sh;
 #pragma unroll
@@ -295,7 +298,12 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
           }
       }
     }
+    if (first_done && lane == 0) first_done[2] = globaltimer() + static_cast<unsigned long long>(acc[0][0][0] * 0.0);
     warp_signal(p, ra, ra + nr, j);
+    if (first_done && lane == 0) {
+      *first_done = globaltimer();
+      first_done = nullptr;
+    }
     if (!more) break;
     if (!pref) {
       if (!strip_deps(p, rn, min(rn + kStrip, r1), j, k, true, true)) return;
@@ -329,6 +337,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
 }
 
 constexpr int kPB = 132;  // doubles per parity of the DIAG publication buffer
+constexpr int kDL = 65;   // row stride of the staged factored tile
 
 // getrf / potrf of one T x T tile (T <= 64) by 8 warps, register resident:
 // warp w owns rows 8w..8w+7, lane l owns columns l and l+32.  Step k needs
@@ -345,7 +354,7 @@ constexpr int kPB = 132;  // doubles per parity of the DIAG publication buffer
 template <bool CHOL>
 __device__ __forceinline__ void tile_factor(double* __restrict__ dk, long long ld, int T, int gcol,
                                             int* info, double* pbuf, double* rk,
-                                            unsigned long long* ph) {
+                                            unsigned long long* ph, double* solve) {
   // pbuf parity block: [0,64) pivot row (LU), [64,128) column k, [128] 1/pivot, [129] l_kk
   // rk[c]: 1/pivot of column c (LU) or 1/l_cc (Cholesky); rk[64 + c]: l_cc
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -380,7 +389,7 @@ __device__ __forceinline__ void tile_factor(double* __restrict__ dk, long long l
       } else {
         if (d <= 0.0) atomicMin(info, gcol);  // kernels.cpp:297-302 (NaN passes)
         const double l0 = sqrt(d);
-        rk[64] = pbuf[129] = l0;
+        rk[64] = l0;
         rk[0] = pbuf[128] = rcp_nr(l0);
       }
     }
@@ -391,49 +400,39 @@ __device__ __forceinline__ void tile_factor(double* __restrict__ dk, long long l
     const double* cb = pbuf + (k & 1) * kPB;
     double* nb = pbuf + ((k + 1) & 1) * kPB;
     const int k1 = k + 1;
-    if (i0 + 7 > k) {  // warp-uniform: this warp still has rows > k
+    if (i0 + 7 > k && i0 < T) {  // warp-uniform: this warp still has live rows > k
+      // x_ij -= a_ik * (u_kj / pivot): the reciprocal is folded into the
+      // operand row (Cholesky: u_kj = a_jk, scaled by 1/l_kk^2), so a step
+      // is one DFMA per element; the multipliers are formed at the end.
       const double r = cb[128];
-      double m[8];
+      const double rs = CHOL ? r * r : r;
+      double a[8];
 #pragma unroll
       for (int q = 0; q < 8; q += 2) {
         const double2 v = *reinterpret_cast<const double2*>(cb + 64 + i0 + q);
-        m[q] = v.x * r;
-        m[q + 1] = v.y * r;
+        a[q] = v.x;
+        a[q + 1] = v.y;
       }
       if (i0 <= k) {  // the warp holding row k: rows <= k are final
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          if (i0 + q <= k) m[q] = 0.0;
+          if (i0 + q <= k) a[q] = 0.0;
       }
-      // operand row: LU pivot row k, Cholesky l_ck = a_ck / l_kk; 0 for columns <= k
       const double* src = CHOL ? cb + 64 : cb;
-      const double sc = CHOL ? r : 1.0;
-      const double u0 = lane > k ? src[lane] * sc : 0.0;
+      const double u0 = lane > k ? src[lane] * rs : 0.0;
       if (wide) {
-        const double u1 = lane + 32 > k ? src[lane + 32] * sc : 0.0;
+        const double u1 = lane + 32 > k ? src[lane + 32] * rs : 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          x[q][0] = fma(-m[q], u0, x[q][0]);
-          x[q][1] = fma(-m[q], u1, x[q][1]);
+          x[q][0] = fma(-a[q], u0, x[q][0]);
+          x[q][1] = fma(-a[q], u1, x[q][1]);
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) x[q][0] = fma(-m[q], u0, x[q][0]);
+        for (int q = 0; q < 8; ++q) x[q][0] = fma(-a[q], u0, x[q][0]);
       }
       if (k1 < T) {
-        // publish column k+1 of my rows (the lane holding it)
-        if (lane == (k1 & 31)) {
-          if (k1 >= 32) {
-#pragma unroll
-            for (int q = 0; q < 8; q += 2)
-              *reinterpret_cast<double2*>(nb + 64 + i0 + q) = make_double2(x[q][1], x[q + 1][1]);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 8; q += 2)
-              *reinterpret_cast<double2*>(nb + 64 + i0 + q) = make_double2(x[q][0], x[q + 1][0]);
-          }
-        }
-        // publish row k+1 (LU) and the next pivot's reciprocal (its owner warp)
+        // next pivot row k+1 (LU) and its reciprocal: the owner warp
         if ((k1 >> 3) == w) {
           const int q1 = k1 & 7;
           double v0 = x[0][0], v1 = x[0][1];
@@ -443,10 +442,6 @@ __device__ __forceinline__ void tile_factor(double* __restrict__ dk, long long l
               v0 = x[q][0];
               v1 = x[q][1];
             }
-          if (!CHOL) {
-            nb[lane] = v0;
-            nb[lane + 32] = v1;
-          }
           if (lane == (k1 & 31)) {
             const double d = k1 >= 32 ? v1 : v0;
             if (!CHOL) {
@@ -455,9 +450,25 @@ __device__ __forceinline__ void tile_factor(double* __restrict__ dk, long long l
             } else {
               if (d <= 0.0) atomicMin(info, gcol + k1);  // kernels.cpp:297-302
               const double l1 = sqrt(d);
-              rk[64 + k1] = nb[129] = l1;
+              rk[64 + k1] = l1;
               rk[k1] = nb[128] = rcp_nr(l1);
             }
+          }
+          if (!CHOL) {
+            nb[lane] = v0;
+            nb[lane + 32] = v1;
+          }
+        }
+        // column k+1 of my rows (the lane holding it)
+        if (lane == (k1 & 31)) {
+          if (k1 >= 32) {
+#pragma unroll
+            for (int q = 0; q < 8; q += 2)
+              *reinterpret_cast<double2*>(nb + 64 + i0 + q) = make_double2(x[q][1], x[q + 1][1]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; q += 2)
+              *reinterpret_cast<double2*>(nb + 64 + i0 + q) = make_double2(x[q][0], x[q + 1][0]);
           }
         }
       }
@@ -472,14 +483,15 @@ __device__ __forceinline__ void tile_factor(double* __restrict__ dk, long long l
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = lane + 32 * h;
-      if (i < T && c < T && (!CHOL || c <= i)) {
-        double v = x[q][h];
-        if (c < i) v *= rk[c];
-        if (CHOL && c == i) v = rk[64 + c];
-        dk[static_cast<long long>(i) * ld + c] = v;
-      }
+      double v = x[q][h];
+      if (c < i) v *= rk[c];
+      if (CHOL && c == i) v = rk[64 + c];
+      if (i < T && c < T && (!CHOL || c <= i)) dk[static_cast<long long>(i) * ld + c] = v;
     }
   }
+  // per-column reciprocals of the diagonal (1/u_cc, Cholesky 1/l_cc) for the
+  // TRSM tasks' 8x8 block inverses
+  if (threadIdx.x < 64) solve[threadIdx.x] = rk[threadIdx.x];
 }
 
 // ---------------------------------------------------------------- TRSM
@@ -571,54 +583,6 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
   }
 }
 
-// Inverse of the 8x8 upper-triangular diagonal block b of Ms (warp b,
-// lanes 0..7 one column each, back substitution) into Minv[b] (row-major).
-__device__ __forceinline__ void block_inverse8(const double* __restrict__ Ms, double* Minv, int b) {
-  const int c = threadIdx.x & 31;
-  if (c < 8) {
-    const double* M = Ms + (b * 8) * kNP + b * 8;
-    double x[8];
-#pragma unroll
-    for (int i = 7; i >= 0; --i) {
-      double s = (i == c) ? 1.0 : 0.0;
-#pragma unroll
-      for (int m = i + 1; m < 8; ++m) s -= M[i * kNP + m] * x[m];
-      x[i] = s / M[i * kNP + i];
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) Minv[b * 64 + i * 8 + c] = x[i];
-  }
-}
-
-// M for the solves, from the factored diagonal tile at `d` (leading dim ld):
-//   upper = true : M = U11 (upper, incl. diagonal)                 LU  L21 solve
-//   upper = false: M = L11^T (n > k from d[n][k]; unit or d[k][k])  LU U12 / Cholesky L21
-__device__ __forceinline__ void load_m(double* Ms, const double* __restrict__ d, long long ld, int T,
-                                       int Tp, bool upper, bool unit) {
-  for (int e = threadIdx.x; e < Tp * Tp; e += kThreads) {
-    int k, c;
-    if (upper) {
-      k = e / Tp;
-      c = e - k * Tp;
-    } else {  // read d row-contiguously: d[c][k]
-      c = e / Tp;
-      k = e - c * Tp;
-    }
-    double v;
-    if (k >= T || c >= T) {
-      v = (k == c) ? 1.0 : 0.0;
-    } else if (c < k) {
-      v = 0.0;
-    } else if (c == k) {
-      v = unit ? 1.0 : __ldcg(d + static_cast<long long>(k) * ld + k);
-    } else {
-      v = upper ? __ldcg(d + static_cast<long long>(k) * ld + c)
-                : __ldcg(d + static_cast<long long>(c) * ld + k);
-    }
-    Ms[k * kNP + c] = v;
-  }
-}
-
 // ---------------------------------------------------------------- kernel
 
 template <int NF, bool CHOL>
@@ -627,8 +591,8 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
   extern __shared__ __align__(16) double dsm[];
   double* sm = dsm;                      // B (GEMM) / M (TRSM): Tp x kNP
   double* abuf = dsm + kSmemB;           // per-warp A strips
-  double* minv = abuf + kSmemA;          // 8 x (8x8) block inverses
-  double* pbuf = minv + 8 * 64;          // DIAG: 2 x kPB
+  double* minv = abuf + kSmemA;          // 8 x (8x8) block inverses + 64 diagonal reciprocals
+  double* pbuf = minv + 9 * 64;          // DIAG: 2 x kPB
   double* rk = pbuf + 2 * kPB;           // DIAG: 128 per-column reciprocals / l_cc
   __shared__ int4 s_task[2];
   __shared__ int s_id[2];
@@ -664,10 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
         s_go = ok;
         s_id[cur ^ 1] = nid;
         s_task[cur ^ 1] = (tk.x >= 0 && nid < p.ntasks) ? p.tasks[nid] : kNone;
-        if (p.trace) {
-          s_t1 = globaltimer();
-          s_ph[2] = clock64();
-        }
+        if (p.trace) s_t1 = globaltimer();
       }
     }
     __syncthreads();
@@ -678,8 +639,11 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
 
     stamp(0);
     stamp(1);
+    stamp(2);
+    stamp(3);
     if (kind == kDiag) {
-      tile_factor<CHOL>(dk, ld, T, kT, p.info, pbuf, rk, p.trace ? s_ph : nullptr);
+      tile_factor<CHOL>(dk, ld, T, kT, p.info, pbuf, rk, p.trace ? s_ph : nullptr,
+                        p.solve + static_cast<long long>(k) * kSolveSlot);
       __threadfence();
       __syncthreads();
       if (tid == 0) {
@@ -692,22 +656,75 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
       // B = U(k, j) (LU) or L(j, k)^T (Cholesky), zero-padded to Tp x Tp
       const double* bsrc = CHOL ? p.a + static_cast<long long>(j * T) * ld + kT
                                 : p.a + static_cast<long long>(kT) * ld + j * T;
-      for (int e = tid; e < Tp * Tp; e += kThreads) {
-        const int x = e / Tp, y = e - x * Tp;  // x: slow index in memory order
-        const double v = (x < T && y < T) ? __ldcg(bsrc + static_cast<long long>(x) * ld + y) : 0.0;
-        if (CHOL)
-          sm[y * kNP + x] = v;  // B[k][n] = L[n][k]
-        else
-          sm[x * kNP + y] = v;
+      {  // all loads in flight before any store: one L2 round trip
+        constexpr int kPer = (Tp * Tp + kThreads - 1) / kThreads;
+        double v[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int e = tid + u * kThreads, x = e / Tp, y = e - x * Tp;  // x: slow index
+          v[u] = (e < Tp * Tp && x < T && y < T) ? __ldcg(bsrc + static_cast<long long>(x) * ld + y)
+                                                 : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int e = tid + u * kThreads, x = e / Tp, y = e - x * Tp;
+          if (e < Tp * Tp) {
+            if (CHOL)
+              sm[y * kNP + x] = v[u];  // B[k][n] = L[n][k]
+            else
+              sm[x * kNP + y] = v[u];
+          }
+        }
       }
       __syncthreads();
-      gemm_strips<NF>(p, r0, r1, k, j, sm, abuf + warp * 2 * kABuf, CHOL);
+      stamp(0);
+      gemm_strips<NF>(p, r0, r1, k, j, sm, abuf + warp * 2 * kABuf, CHOL,
+                      (p.trace && warp == 0) ? &s_ph[1] : nullptr);
     } else {  // TRSM
       const bool lsolve = kind == kTrsmL;
-      load_m(sm, dk, ld, T, Tp, !CHOL && lsolve, !CHOL && !lsolve);
+      {  // M from the factored diagonal tile (one batched L2 round trip), then
+         // the inverses of its 8x8 diagonal blocks (no divisions: DIAG(k)
+         // published the diagonal reciprocals)
+        const bool upper = !CHOL && lsolve, unit = !CHOL && !lsolve;
+        constexpr int kPer = (Tp * Tp + kThreads - 1) / kThreads;
+        double v[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {  // element (x, y) of the tile, row-contiguous
+          const int e = tid + u * kThreads, x = e / Tp, y = e - x * Tp;
+          const bool need = e < Tp * Tp && x < T && y < T && (upper ? y > x : y < x);
+          v[u] = need ? __ldcg(dk + static_cast<long long>(x) * ld + y) : 0.0;
+        }
+        const double* rdg = p.solve + static_cast<long long>(k) * kSolveSlot;
+        if (tid < Tp) minv[8 * 64 + tid] = tid < T ? __ldcg(rdg + tid) : 1.0;  // 1/diag
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int e = tid + u * kThreads, x = e / Tp, y = e - x * Tp;
+          if (e < Tp * Tp) {
+            // M[kk][c]: U11 (upper) or L11^T; diagonal: 1 if unit / padding, else 1/rdiag
+            if (upper) sm[x * kNP + y] = v[u];
+            else sm[y * kNP + x] = v[u];
+          }
+        }
+        __syncthreads();  // (M's diagonal is never read: the solve applies inv(M_bb))
+        const int job = tid >> 3, c = tid & 7;
+        if (job < NF) {  // inverse of block `job`, column c: back substitution
+          const int b = job;
+          double xr[8];
+#pragma unroll
+          for (int ii = 7; ii >= 0; --ii) {
+            double acc = ii == c ? 1.0 : 0.0;
+#pragma unroll
+            for (int m = ii + 1; m < 8; ++m) acc = fma(-sm[(8 * b + ii) * kNP + 8 * b + m], xr[m], acc);
+            const int gi = 8 * b + ii;
+            xr[ii] = acc * ((unit || gi >= T) ? 1.0 : minv[8 * 64 + gi]);
+          }
+#pragma unroll
+          for (int ii = 0; ii < 8; ++ii) minv[b * 64 + ii * 8 + c] = xr[ii];
+        }
+      }
       __syncthreads();
-      if (warp < NF) block_inverse8(sm, minv, warp);
-      __syncthreads();
+      stamp(0);
+      stamp(1);
       if (lsolve) {
         for (int ra = r0 + warp * kStrip; ra < r1; ra += kWarps * kStrip) {
           const int nr = min(kStrip, r1 - ra);
@@ -734,7 +751,6 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
       tr[1] = s_t1;
       tr[2] = globaltimer();
       tr[3] = smid;
-      s_ph[3] = clock64();
       tr[4] = s_ph[0];
       tr[5] = s_ph[1];
       tr[6] = s_ph[2];
@@ -834,6 +850,8 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   if (e != cudaSuccess) return e;
   e = cudaMalloc(&w->cnt, w->cnt_bytes);
   if (e != cudaSuccess) return e;
+  e = cudaMalloc(&w->solve, static_cast<size_t>(nt) * kSolveSlot * sizeof(double));
+  if (e != cudaSuccess) return e;
   const char* tr = std::getenv("TT_DAG_TRACE");
   if (tr && tr[0] == '1') {
     e = cudaMalloc(&w->trace, tasks.size() * 8 * sizeof(unsigned long long));
@@ -850,6 +868,7 @@ void destroy(Workspace* w) {
   if (w->tasks) cudaFree(w->tasks);
   if (w->cnt) cudaFree(w->cnt);
   if (w->trace) cudaFree(w->trace);
+  if (w->solve) cudaFree(w->solve);
   *w = Workspace{};
 }
 
@@ -871,6 +890,7 @@ cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long l
   prm.abort = prm.next + 1;
   prm.info = info;
   prm.trace = w.trace;
+  prm.solve = w.solve;
   const int nf = (bx + 7) / 8;
   return chol ? launch_nf<true>(nf, prm, w.grid, s) : launch_nf<false>(nf, prm, w.grid, s);
 }

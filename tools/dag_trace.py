@@ -42,10 +42,15 @@ dm = kind == 0
 ph = (tr[dm, 4:6].astype(np.int64) - t0) / 1e3
 print("  DIAG phases (us after ready): load+sync %.2f, loop %.2f, rest %.2f" % (
     (ph[:, 0] - t[dm, 1]).mean(), (ph[:, 1] - ph[:, 0]).mean(), (t[dm, 2] - ph[:, 1]).mean()))
-cyc = tr[:, 7].astype(np.int64) - tr[:, 6].astype(np.int64)
-ns = tr[:, 2].astype(np.int64) - tr[:, 1].astype(np.int64)
-ok = ns > 2000
-print("  effective SM clock during tasks: %.3f GHz (median)" % np.median(cyc[ok] / ns[ok]))
+for kk, nm, a_, b_ in [(2, "TRSM_U", "M load+sync", "8x8 inverses+sync"), (1, "TRSM_L", "M load+sync", "8x8 inverses+sync"), (3, "GEMM", "B load+sync", "first strip (warp 0) done")]:
+    mm = kind == kk
+    if mm.any():
+        q = (tr[mm, 4:6].astype(np.int64) - t0) / 1e3
+        print(f"  {nm} phases (us after ready): {a_} {(q[:, 0] - t[mm, 1]).mean():.2f}, {b_} +{(q[:, 1] - q[:, 0]).mean():.2f}, end +{(t[mm, 2] - q[:, 1]).mean():.2f}")
+mm = kind == 3
+q = (tr[mm, 4:8].astype(np.int64) - t0) / 1e3
+print("  GEMM first strip (warp 0): data ready +%.2f, computed+stored +%.2f, fence+signal +%.2f us" % (
+    (q[:, 2] - q[:, 0]).mean(), (q[:, 3] - q[:, 2]).mean(), (q[:, 1] - q[:, 3]).mean()))
 busy = (t[:, 2] - t[:, 1]).sum()
 grid = len(set(tr[:, 3]))
 print(f"  utilisation (task run time / (SMs x span)) = {busy / (grid * span):.3f}")

@@ -1,0 +1,4 @@
+for c in "lu 2000 400 50" "lu 2000 100 40"; do
+  set -- $c
+  timeout -s KILL 120 python tools/dag_trace.py $c gpurun_out/trace_$1_$2_$3_$4.npz 2>&1 | grep -v "    k="
+done
