@@ -337,7 +337,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
 }
 
 constexpr int kPB = 132;  // doubles per parity of the DIAG publication buffer
-constexpr int kDL = 65;   // row stride of the staged factored tile
+
 
 // getrf / potrf of one T x T tile (T <= 64) by 8 warps, register resident:
 // warp w owns rows 8w..8w+7, lane l owns columns l and l+32.  Step k needs
@@ -432,26 +432,29 @@ __device__ __forceinline__ void tile_factor(double* __restrict__ dk, long long l
         for (int q = 0; q < 8; ++q) x[q][0] = fma(-a[q], u0, x[q][0]);
       }
       if (k1 < T) {
-        // next pivot row k+1 (LU) and its reciprocal: the owner warp
+        // next pivot row k+1 (LU) and its reciprocal: the owner warp (a
+        // uniform jump on q1 = (k+1) % 8 instead of a select chain)
         if ((k1 >> 3) == w) {
-          const int q1 = k1 & 7;
-          double v0 = x[0][0], v1 = x[0][1];
-#pragma unroll
-          for (int q = 1; q < 8; ++q)
-            if (q == q1) {
-              v0 = x[q][0];
-              v1 = x[q][1];
-            }
+          double v0, v1;
+          switch (k1 & 7) {
+#define TT_ROW(Q)     \
+  case Q:             \
+    v0 = x[Q][0];     \
+    v1 = x[Q][1];     \
+    break;
+            TT_ROW(0) TT_ROW(1) TT_ROW(2) TT_ROW(3) TT_ROW(4) TT_ROW(5) TT_ROW(6) default: TT_ROW(7)
+#undef TT_ROW
+          }
           if (lane == (k1 & 31)) {
             const double d = k1 >= 32 ? v1 : v0;
             if (!CHOL) {
-              if (fabs(d) < 1e-300) atomicMin(info, gcol + k1);  // kernels.cpp:187-190
               rk[k1] = nb[128] = rcp_nr(d);
+              if (fabs(d) < 1e-300) atomicMin(info, gcol + k1);  // kernels.cpp:187-190
             } else {
-              if (d <= 0.0) atomicMin(info, gcol + k1);  // kernels.cpp:297-302
               const double l1 = sqrt(d);
               rk[64 + k1] = l1;
               rk[k1] = nb[128] = rcp_nr(l1);
+              if (d <= 0.0) atomicMin(info, gcol + k1);  // kernels.cpp:297-302
             }
           }
           if (!CHOL) {
@@ -492,6 +495,189 @@ __device__ __forceinline__ void tile_factor(double* __restrict__ dk, long long l
   // per-column reciprocals of the diagonal (1/u_cc, Cholesky 1/l_cc) for the
   // TRSM tasks' 8x8 block inverses
   if (threadIdx.x < 64) solve[threadIdx.x] = rk[threadIdx.x];
+}
+
+// Blocked factorisation of the diagonal tile (T <= 64, NB = ceil(T/8) blocks),
+// the tile resident in shared memory D (64 x kNP, identity-padded):
+//   per 8-column block b:  warp 0 factors the 8x8 diagonal block in DMMA
+//   fragment layout with shuffles (the only per-pivot serial chain: shuffle,
+//   reciprocal, multiply, FMA) and forms inv(U_bb), inv(L_bb); then all
+//   warps solve the L and U panels (X = A inv(U_bb), Y = inv(L_bb) A) and
+//   apply the rank-8 trailing update on the fp64 tensor cores (DMMA 8x8x4).
+// Three __syncthreads per 8 pivots instead of one per pivot.  Cholesky runs
+// the same elimination on the symmetric tile (A = L U with U = diag(u) L^T)
+// and scales: l_ij = L_ij sqrt(u_jj).  Failure predicates are the
+// reference's on the same Schur-complement pivots (kernels.cpp:187-190,
+// :297-302; NaN passes).
+template <bool CHOL>
+__device__ __forceinline__ void tile_factor_blocked(double* __restrict__ dk, long long ld, int T,
+                                                    int gcol, int* info, double* D, double* inv,
+                                                    double* rk, unsigned long long* ph,
+                                                    double* solve) {
+  // inv: [0,64) inv(U_bb) row-major, [64,128) inv(L_bb); rk: 64 reciprocals of u_jj
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int NB = (T + 7) >> 3, Tp = NB * 8;
+  {  // load (Cholesky: mirror the lower triangle), identity padding
+    constexpr int kPer = 64 * 64 / kThreads;
+    double v[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = tid + u * kThreads, i = e >> 6, c = e & 63;
+      const int si = (CHOL && c > i) ? c : i, sc = (CHOL && c > i) ? i : c;
+      v[u] = (i < T && c < T) ? __ldcg(dk + static_cast<long long>(si) * ld + sc)
+                              : (i == c ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = tid + u * kThreads;
+      D[(e >> 6) * kNP + (e & 63)] = v[u];
+    }
+  }
+  __syncthreads();
+  if (ph && tid == 0) ph[0] = globaltimer();
+  for (int b = 0; b < NB; ++b) {
+    const int p = 8 * b;
+    if (warp == 0) {
+      __syncwarp();  // converged warp: keeps the shuffles on the fast (non-divergent) path
+      // ---- 8x8 diagonal block, lane (g,t) holds (g, 2t), (g, 2t+1)
+      double v0 = D[(p + g) * kNP + p + 2 * t], v1 = D[(p + g) * kNP + p + 2 * t + 1];
+      double rr[8], pv[8];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const double sel = (kk & 1) ? v1 : v0;
+        const double piv = __shfl_sync(0xffffffffu, sel, kk * 4 + (kk >> 1));
+        const double agk = __shfl_sync(0xffffffffu, sel, g * 4 + (kk >> 1));
+        const double u0 = __shfl_sync(0xffffffffu, v0, kk * 4 + t);
+        const double u1 = __shfl_sync(0xffffffffu, v1, kk * 4 + t);
+        const double r = rcp_nr(piv);
+        const double m = g > kk ? agk * r : 0.0;
+        if (2 * t > kk) v0 = fma(-m, u0, v0);
+        if (2 * t + 1 > kk) v1 = fma(-m, u1, v1);
+        if (g > kk && 2 * t == kk) v0 = m;
+        if (g > kk && 2 * t + 1 == kk) v1 = m;
+        rr[kk] = r;
+        pv[kk] = piv;
+      }
+      D[(p + g) * kNP + p + 2 * t] = v0;
+      D[(p + g) * kNP + p + 2 * t + 1] = v1;
+      // reciprocals for the solves and the reference's failure predicates,
+      // off the pivot chain (lane kk handles pivot kk)
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        if (lane == kk && p + kk < T) {
+          rk[p + kk] = rr[kk];
+          const double piv = pv[kk];
+          if (CHOL ? piv <= 0.0 : fabs(piv) < 1e-300)
+            atomicMin(info, gcol + p + kk);  // kernels.cpp:187-190 / :297-302 (NaN passes)
+        }
+      }
+      __syncwarp();
+      // inv(U_bb): lanes 0..7 (column c, back substitution); inv(L_bb) (unit
+      // lower): lanes 8..15 (column c, forward substitution)
+      if (lane < 16) {
+        const int c = lane & 7;
+        double x[8];
+        if (lane < 8) {
+#pragma unroll
+          for (int ii = 7; ii >= 0; --ii) {
+            double acc = ii == c ? 1.0 : 0.0;
+#pragma unroll
+            for (int mm = ii + 1; mm < 8; ++mm) acc = fma(-D[(p + ii) * kNP + p + mm], x[mm], acc);
+            x[ii] = acc * (p + ii < T ? rk[p + ii] : 1.0);
+          }
+#pragma unroll
+          for (int ii = 0; ii < 8; ++ii) inv[ii * 8 + c] = x[ii];
+        } else {
+#pragma unroll
+          for (int ii = 0; ii < 8; ++ii) {
+            double acc = ii == c ? 1.0 : 0.0;
+#pragma unroll
+            for (int mm = 0; mm < ii; ++mm) acc = fma(-D[(p + ii) * kNP + p + mm], x[mm], acc);
+            x[ii] = acc;
+          }
+#pragma unroll
+          for (int ii = 0; ii < 8; ++ii) inv[64 + ii * 8 + c] = x[ii];
+        }
+      }
+    }
+    __syncthreads();
+    const int nr = NB - b - 1;  // blocks beyond the diagonal one
+    if (nr == 0) break;
+    // ---- panels: job < nr: L block (b+1+job, b) = A * inv(U_bb);
+    //               job >= nr: U block (b, b+1+job-nr) = inv(L_bb) * A
+    for (int job = warp; job < 2 * nr; job += kWarps) {
+      double c0 = 0.0, c1 = 0.0;
+      if (job < nr) {
+        const int rb = 8 * (b + 1 + job);
+        const double a0 = D[(rb + g) * kNP + p + t], a1 = D[(rb + g) * kNP + p + 4 + t];
+        const double b0 = inv[t * 8 + g], b1 = inv[(4 + t) * 8 + g];
+        dmma_8x8x4(c0, c1, a0, b0);
+        dmma_8x8x4(c0, c1, a1, b1);
+        __syncwarp();
+        D[(rb + g) * kNP + p + 2 * t] = c0;
+        D[(rb + g) * kNP + p + 2 * t + 1] = c1;
+      } else {
+        const int cb = 8 * (b + 1 + job - nr);
+        const double a0 = inv[64 + g * 8 + t], a1 = inv[64 + g * 8 + 4 + t];
+        const double b0 = D[(p + t) * kNP + cb + g], b1 = D[(p + 4 + t) * kNP + cb + g];
+        dmma_8x8x4(c0, c1, a0, b0);
+        dmma_8x8x4(c0, c1, a1, b1);
+        __syncwarp();
+        D[(p + g) * kNP + cb + 2 * t] = c0;
+        D[(p + g) * kNP + cb + 2 * t + 1] = c1;
+      }
+    }
+    __syncthreads();
+    // ---- trailing update: block (ib, jb) -= L(ib, b) * U(b, jb); warp w
+    // owns block row b+1+w (A fragments loaded once, all jb loads in flight)
+    for (int ir = warp; ir < nr; ir += kWarps) {
+      const int ib = 8 * (b + 1 + ir);
+      const double a0 = -D[(ib + g) * kNP + p + t], a1 = -D[(ib + g) * kNP + p + 4 + t];
+      double c0[7], c1[7];
+#pragma unroll
+      for (int jr = 0; jr < 7; ++jr) {
+        if (jr < nr) {
+          const int jb = 8 * (b + 1 + jr);
+          c0[jr] = D[(ib + g) * kNP + jb + 2 * t];
+          c1[jr] = D[(ib + g) * kNP + jb + 2 * t + 1];
+          const double b0 = D[(p + t) * kNP + jb + g], b1 = D[(p + 4 + t) * kNP + jb + g];
+          dmma_8x8x4(c0[jr], c1[jr], a0, b0);
+          dmma_8x8x4(c0[jr], c1[jr], a1, b1);
+        }
+      }
+#pragma unroll
+      for (int jr = 0; jr < 7; ++jr) {
+        if (jr < nr) {
+          const int jb = 8 * (b + 1 + jr);
+          D[(ib + g) * kNP + jb + 2 * t] = c0[jr];
+          D[(ib + g) * kNP + jb + 2 * t + 1] = c1[jr];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (ph && tid == 0) ph[1] = globaltimer();
+  // Cholesky: l_jj = sqrt(u_jj), 1/l_jj for the solves
+  if (CHOL && tid < T) {
+    const double l = sqrt(D[tid * kNP + tid]);
+    rk[64 + tid] = l;
+    rk[tid] = rcp_nr(l);
+  }
+  if (CHOL) __syncthreads();
+  {  // store the factored tile (Cholesky: lower only, scaled)
+    constexpr int kPer = 64 * 64 / kThreads;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = tid + u * kThreads, i = e >> 6, c = e & 63;
+      if (i < T && c < T && (!CHOL || c <= i)) {
+        double v = D[i * kNP + c];
+        if (CHOL) v = c == i ? rk[64 + c] : v * rk[64 + c];
+        dk[static_cast<long long>(i) * ld + c] = v;
+      }
+    }
+  }
+  if (tid < 64) solve[tid] = rk[tid];
+  (void)Tp;
 }
 
 // ---------------------------------------------------------------- TRSM
@@ -642,8 +828,8 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
     stamp(2);
     stamp(3);
     if (kind == kDiag) {
-      tile_factor<CHOL>(dk, ld, T, kT, p.info, pbuf, rk, p.trace ? s_ph : nullptr,
-                        p.solve + static_cast<long long>(k) * kSolveSlot);
+      tile_factor_blocked<CHOL>(dk, ld, T, kT, p.info, sm, pbuf, rk, p.trace ? s_ph : nullptr,
+                                p.solve + static_cast<long long>(k) * kSolveSlot);
       __threadfence();
       __syncthreads();
       if (tid == 0) {
