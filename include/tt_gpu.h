@@ -148,8 +148,9 @@ int tt_dag_tasks(int kernel, int n, int by, int bx, int* out, int cap);
 /* With TT_DAG_TRACE=1 in the environment the persistent schedule records,
  * per task, {fetch, dependencies-ready, done} (%globaltimer ns) and the SM
  * id and four phase stamps; this copies the most recently run schedule's
- * trace (8 u64 per task, in task-list order) and returns the task count
- * (-1: no trace). */
+ * trace (8 u64 per task, in task-list order, then one row per walker step:
+ * start, tile ready, updated, factored, panel ready, panel published) and
+ * returns the row count (-1: no trace). */
 int tt_dag_trace(tt_ctx* ctx, unsigned long long* out, int cap);
 
 /* Counter of kernel launches issued by this context (graph nodes count once

@@ -43,7 +43,9 @@ constexpr int kAW = 68;
 constexpr int kABuf = kStrip * kAW;              // doubles per buffer
 constexpr int kSmemB = kIB * kNP;                // B / M tile
 constexpr int kSmemA = kWarps * 2 * kABuf;       // all warps' A buffers
-constexpr int kSmemBytes = (kSmemB + kSmemA + 9 * 64 + 2 * 132 + 128) * 8;
+// walker-only: DIAG block inverses (1024) + the U12-solve block inverses (512)
+constexpr int kSmemW = 1536;
+constexpr int kSmemBytes = (kSmemB + kSmemA + 9 * 64 + 2 * 132 + 128 + kSmemW) * 8;
 constexpr int kSolveSlot = 64;  // per step: diagonal reciprocals written by DIAG
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -339,206 +341,51 @@ __device__ __forceinline__ double rcp_nr(double x) {
 constexpr int kPB = 132;  // doubles per parity of the DIAG publication buffer
 
 
-// getrf / potrf of one T x T tile (T <= 64) by 8 warps, register resident:
-// warp w owns rows 8w..8w+7, lane l owns columns l and l+32.  Step k needs
-// the final pivot row k (LU), column k and the reciprocal of the pivot,
-// which their owners publish in shared memory at the end of step k-1
-// (double-buffered by step parity; one __syncthreads per pivot).  Warps
-// whose rows are all finished skip the step; T <= 32 skips the upper column
-// half.  The step is branch- and select-free for all but the warp holding
-// row k: columns <= k see a zero operand (x - m*0 = x), and the multipliers
-// l_ik = a_ik * (1/a_kk) are formed once at the end from the per-column
-// reciprocals (column k is never touched after step k).  Per element the
-// reference panel's operation order (kernels.cpp:186-196 / :289-306); the
-// reciprocal-multiply is <= 1 ulp from the reference's division.
-template <bool CHOL>
-__device__ __forceinline__ void tile_factor(double* __restrict__ dk, long long ld, int T, int gcol,
-                                            int* info, double* pbuf, double* rk,
-                                            unsigned long long* ph, double* solve) {
-  // pbuf parity block: [0,64) pivot row (LU), [64,128) column k, [128] 1/pivot, [129] l_kk
-  // rk[c]: 1/pivot of column c (LU) or 1/l_cc (Cholesky); rk[64 + c]: l_cc
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i0 = 8 * w;
-  const bool wide = T > 32;
-  double x[8][2];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int i = i0 + q;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = lane + 32 * h;
-      x[q][h] = (i < T && c < T && (!CHOL || c <= i))
-                    ? __ldcg(dk + static_cast<long long>(i) * ld + c) : 0.0;
-    }
-  }
-  // publish step 0: column 0 (+ row 0 for LU) and the pivot's reciprocal
-  if (lane == 0) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) pbuf[64 + i0 + q] = x[q][0];
-  }
-  if (w == 0) {
-    if (!CHOL) {
-      pbuf[lane] = x[0][0];
-      pbuf[lane + 32] = x[0][1];
-    }
-    if (lane == 0) {
-      const double d = x[0][0];
-      if (!CHOL) {
-        if (fabs(d) < 1e-300) atomicMin(info, gcol);  // kernels.cpp:187-190
-        rk[0] = pbuf[128] = rcp_nr(d);
-      } else {
-        if (d <= 0.0) atomicMin(info, gcol);  // kernels.cpp:297-302 (NaN passes)
-        const double l0 = sqrt(d);
-        rk[64] = l0;
-        rk[0] = pbuf[128] = rcp_nr(l0);
-      }
-    }
-  }
-  __syncthreads();
-  if (ph && threadIdx.x == 0) ph[0] = globaltimer();
-  for (int k = 0; k < T; ++k) {
-    const double* cb = pbuf + (k & 1) * kPB;
-    double* nb = pbuf + ((k + 1) & 1) * kPB;
-    const int k1 = k + 1;
-    if (i0 + 7 > k && i0 < T) {  // warp-uniform: this warp still has live rows > k
-      // x_ij -= a_ik * (u_kj / pivot): the reciprocal is folded into the
-      // operand row (Cholesky: u_kj = a_jk, scaled by 1/l_kk^2), so a step
-      // is one DFMA per element; the multipliers are formed at the end.
-      const double r = cb[128];
-      const double rs = CHOL ? r * r : r;
-      double a[8];
-#pragma unroll
-      for (int q = 0; q < 8; q += 2) {
-        const double2 v = *reinterpret_cast<const double2*>(cb + 64 + i0 + q);
-        a[q] = v.x;
-        a[q + 1] = v.y;
-      }
-      if (i0 <= k) {  // the warp holding row k: rows <= k are final
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (i0 + q <= k) a[q] = 0.0;
-      }
-      const double* src = CHOL ? cb + 64 : cb;
-      const double u0 = lane > k ? src[lane] * rs : 0.0;
-      if (wide) {
-        const double u1 = lane + 32 > k ? src[lane + 32] * rs : 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          x[q][0] = fma(-a[q], u0, x[q][0]);
-          x[q][1] = fma(-a[q], u1, x[q][1]);
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) x[q][0] = fma(-a[q], u0, x[q][0]);
-      }
-      if (k1 < T) {
-        // next pivot row k+1 (LU) and its reciprocal: the owner warp (a
-        // uniform jump on q1 = (k+1) % 8 instead of a select chain)
-        if ((k1 >> 3) == w) {
-          double v0, v1;
-          switch (k1 & 7) {
-#define TT_ROW(Q)     \
-  case Q:             \
-    v0 = x[Q][0];     \
-    v1 = x[Q][1];     \
-    break;
-            TT_ROW(0) TT_ROW(1) TT_ROW(2) TT_ROW(3) TT_ROW(4) TT_ROW(5) TT_ROW(6) default: TT_ROW(7)
-#undef TT_ROW
-          }
-          if (lane == (k1 & 31)) {
-            const double d = k1 >= 32 ? v1 : v0;
-            if (!CHOL) {
-              rk[k1] = nb[128] = rcp_nr(d);
-              if (fabs(d) < 1e-300) atomicMin(info, gcol + k1);  // kernels.cpp:187-190
-            } else {
-              const double l1 = sqrt(d);
-              rk[64 + k1] = l1;
-              rk[k1] = nb[128] = rcp_nr(l1);
-              if (d <= 0.0) atomicMin(info, gcol + k1);  // kernels.cpp:297-302
-            }
-          }
-          if (!CHOL) {
-            nb[lane] = v0;
-            nb[lane + 32] = v1;
-          }
-        }
-        // column k+1 of my rows (the lane holding it)
-        if (lane == (k1 & 31)) {
-          if (k1 >= 32) {
-#pragma unroll
-            for (int q = 0; q < 8; q += 2)
-              *reinterpret_cast<double2*>(nb + 64 + i0 + q) = make_double2(x[q][1], x[q + 1][1]);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 8; q += 2)
-              *reinterpret_cast<double2*>(nb + 64 + i0 + q) = make_double2(x[q][0], x[q + 1][0]);
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (ph && threadIdx.x == 0) ph[1] = globaltimer();
-  // multipliers below the diagonal (and l_cc on it for Cholesky), then store
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int i = i0 + q;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = lane + 32 * h;
-      double v = x[q][h];
-      if (c < i) v *= rk[c];
-      if (CHOL && c == i) v = rk[64 + c];
-      if (i < T && c < T && (!CHOL || c <= i)) dk[static_cast<long long>(i) * ld + c] = v;
-    }
-  }
-  // per-column reciprocals of the diagonal (1/u_cc, Cholesky 1/l_cc) for the
-  // TRSM tasks' 8x8 block inverses
-  if (threadIdx.x < 64) solve[threadIdx.x] = rk[threadIdx.x];
-}
-
-// Blocked factorisation of the diagonal tile (T <= 64, NB = ceil(T/8) blocks),
-// the tile resident in shared memory D (64 x kNP, identity-padded):
+// Blocked factorisation of the diagonal tile (T <= 64, NB = ceil(T/8) blocks)
+// resident in shared memory D (64 x kNP, identity-padded):
 //   per 8-column block b:  warp 0 factors the 8x8 diagonal block in DMMA
 //   fragment layout with shuffles (the only per-pivot serial chain: shuffle,
-//   reciprocal, multiply, FMA) and forms inv(U_bb), inv(L_bb); then all
-//   warps solve the L and U panels (X = A inv(U_bb), Y = inv(L_bb) A) and
-//   apply the rank-8 trailing update on the fp64 tensor cores (DMMA 8x8x4).
+//   reciprocal, multiply, FMA) and forms inv(U_bb), inv(L_bb) (kept in
+//   `inv` for the solves); then all warps solve the L and U panels
+//   (X = A inv(U_bb), Y = inv(L_bb) A) and apply the rank-8 trailing update
+//   on the fp64 tensor cores (DMMA 8x8x4).
 // Three __syncthreads per 8 pivots instead of one per pivot.  Cholesky runs
-// the same elimination on the symmetric tile (A = L U with U = diag(u) L^T)
-// and scales: l_ij = L_ij sqrt(u_jj).  Failure predicates are the
+// the same elimination on the symmetric tile (A = L U with U = diag(u) L^T);
+// tile_store scales l_ij = L_ij sqrt(u_jj).  Failure predicates are the
 // reference's on the same Schur-complement pivots (kernels.cpp:187-190,
 // :297-302; NaN passes).
+// inv: [b*64, +64) inv(U_bb) row-major, [512 + b*64, +64) inv(L_bb) row-major.
+// rk[c] = 1/u_cc.
 template <bool CHOL>
-__device__ __forceinline__ void tile_factor_blocked(double* __restrict__ dk, long long ld, int T,
-                                                    int gcol, int* info, double* D, double* inv,
-                                                    double* rk, unsigned long long* ph,
-                                                    double* solve) {
-  // inv: [0,64) inv(U_bb) row-major, [64,128) inv(L_bb); rk: 64 reciprocals of u_jj
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int NB = (T + 7) >> 3, Tp = NB * 8;
-  {  // load (Cholesky: mirror the lower triangle), identity padding
-    constexpr int kPer = 64 * 64 / kThreads;
-    double v[kPer];
+__device__ __forceinline__ void tile_load(double* D, const double* __restrict__ dk, long long ld,
+                                          int T) {
+  constexpr int kPer = 64 * 64 / kThreads;
+  double v[kPer];
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int e = tid + u * kThreads, i = e >> 6, c = e & 63;
-      const int si = (CHOL && c > i) ? c : i, sc = (CHOL && c > i) ? i : c;
-      v[u] = (i < T && c < T) ? __ldcg(dk + static_cast<long long>(si) * ld + sc)
-                              : (i == c ? 1.0 : 0.0);
-    }
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int e = tid + u * kThreads;
-      D[(e >> 6) * kNP + (e & 63)] = v[u];
-    }
+  for (int u = 0; u < kPer; ++u) {  // Cholesky: mirror the lower triangle
+    const int e = threadIdx.x + u * kThreads, i = e >> 6, c = e & 63;
+    const int si = (CHOL && c > i) ? c : i, sc = (CHOL && c > i) ? i : c;
+    v[u] = (i < T && c < T) ? __ldcg(dk + static_cast<long long>(si) * ld + sc)
+                            : (i == c ? 1.0 : 0.0);
   }
-  __syncthreads();
-  if (ph && tid == 0) ph[0] = globaltimer();
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = threadIdx.x + u * kThreads;
+    D[(e >> 6) * kNP + (e & 63)] = v[u];
+  }
+}
+
+template <bool CHOL>
+__device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* info, double* inv,
+                                             double* rk) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int NB = (T + 7) >> 3;
   for (int b = 0; b < NB; ++b) {
     const int p = 8 * b;
+    double* invU = inv + b * 64;
+    double* invL = inv + 512 + b * 64;
     if (warp == 0) {
-      __syncwarp();  // converged warp: keeps the shuffles on the fast (non-divergent) path
+      __syncwarp();  // converged warp: keeps the shuffles on the fast path
       // ---- 8x8 diagonal block, lane (g,t) holds (g, 2t), (g, 2t+1)
       double v0 = D[(p + g) * kNP + p + 2 * t], v1 = D[(p + g) * kNP + p + 2 * t + 1];
       double rr[8], pv[8];
@@ -560,8 +407,7 @@ __device__ __forceinline__ void tile_factor_blocked(double* __restrict__ dk, lon
       }
       D[(p + g) * kNP + p + 2 * t] = v0;
       D[(p + g) * kNP + p + 2 * t + 1] = v1;
-      // reciprocals for the solves and the reference's failure predicates,
-      // off the pivot chain (lane kk handles pivot kk)
+      // reciprocals and the reference's failure predicates, off the pivot chain
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         if (lane == kk && p + kk < T) {
@@ -586,7 +432,7 @@ __device__ __forceinline__ void tile_factor_blocked(double* __restrict__ dk, lon
             x[ii] = acc * (p + ii < T ? rk[p + ii] : 1.0);
           }
 #pragma unroll
-          for (int ii = 0; ii < 8; ++ii) inv[ii * 8 + c] = x[ii];
+          for (int ii = 0; ii < 8; ++ii) invU[ii * 8 + c] = x[ii];
         } else {
 #pragma unroll
           for (int ii = 0; ii < 8; ++ii) {
@@ -596,7 +442,7 @@ __device__ __forceinline__ void tile_factor_blocked(double* __restrict__ dk, lon
             x[ii] = acc;
           }
 #pragma unroll
-          for (int ii = 0; ii < 8; ++ii) inv[64 + ii * 8 + c] = x[ii];
+          for (int ii = 0; ii < 8; ++ii) invL[ii * 8 + c] = x[ii];
         }
       }
     }
@@ -610,7 +456,7 @@ __device__ __forceinline__ void tile_factor_blocked(double* __restrict__ dk, lon
       if (job < nr) {
         const int rb = 8 * (b + 1 + job);
         const double a0 = D[(rb + g) * kNP + p + t], a1 = D[(rb + g) * kNP + p + 4 + t];
-        const double b0 = inv[t * 8 + g], b1 = inv[(4 + t) * 8 + g];
+        const double b0 = invU[t * 8 + g], b1 = invU[(4 + t) * 8 + g];
         dmma_8x8x4(c0, c1, a0, b0);
         dmma_8x8x4(c0, c1, a1, b1);
         __syncwarp();
@@ -618,7 +464,7 @@ __device__ __forceinline__ void tile_factor_blocked(double* __restrict__ dk, lon
         D[(rb + g) * kNP + p + 2 * t + 1] = c1;
       } else {
         const int cb = 8 * (b + 1 + job - nr);
-        const double a0 = inv[64 + g * 8 + t], a1 = inv[64 + g * 8 + 4 + t];
+        const double a0 = invL[g * 8 + t], a1 = invL[g * 8 + 4 + t];
         const double b0 = D[(p + t) * kNP + cb + g], b1 = D[(p + 4 + t) * kNP + cb + g];
         dmma_8x8x4(c0, c1, a0, b0);
         dmma_8x8x4(c0, c1, a1, b1);
@@ -656,28 +502,31 @@ __device__ __forceinline__ void tile_factor_blocked(double* __restrict__ dk, lon
     }
     __syncthreads();
   }
-  if (ph && tid == 0) ph[1] = globaltimer();
-  // Cholesky: l_jj = sqrt(u_jj), 1/l_jj for the solves
+  // Cholesky: l_jj = sqrt(u_jj) (rk[64 + j]) and 1/l_jj (rk[j]) for the solves
   if (CHOL && tid < T) {
     const double l = sqrt(D[tid * kNP + tid]);
     rk[64 + tid] = l;
     rk[tid] = rcp_nr(l);
   }
-  if (CHOL) __syncthreads();
-  {  // store the factored tile (Cholesky: lower only, scaled)
-    constexpr int kPer = 64 * 64 / kThreads;
+  __syncthreads();
+}
+
+// Factored tile -> global (Cholesky: lower only, scaled) and the diagonal
+// reciprocals -> the step's solve slot (read by the TRSM tasks).
+template <bool CHOL>
+__device__ __forceinline__ void tile_store(const double* D, double* __restrict__ dk, long long ld,
+                                           int T, const double* rk, double* solve) {
+  constexpr int kPer = 64 * 64 / kThreads;
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int e = tid + u * kThreads, i = e >> 6, c = e & 63;
-      if (i < T && c < T && (!CHOL || c <= i)) {
-        double v = D[i * kNP + c];
-        if (CHOL) v = c == i ? rk[64 + c] : v * rk[64 + c];
-        dk[static_cast<long long>(i) * ld + c] = v;
-      }
+  for (int u = 0; u < kPer; ++u) {
+    const int e = threadIdx.x + u * kThreads, i = e >> 6, c = e & 63;
+    if (i < T && c < T && (!CHOL || c <= i)) {
+      double v = D[i * kNP + c];
+      if (CHOL) v = c == i ? rk[64 + c] : v * rk[64 + c];
+      dk[static_cast<long long>(i) * ld + c] = v;
     }
   }
-  if (tid < 64) solve[tid] = rk[tid];
-  (void)Tp;
+  if (threadIdx.x < 64) solve[threadIdx.x] = rk[threadIdx.x];
 }
 
 // ---------------------------------------------------------------- TRSM
@@ -686,7 +535,7 @@ __device__ __forceinline__ void tile_factor_blocked(double* __restrict__ dk, lon
 // transposed U12 solve).  M (Tp x Tp upper triangular, identity-padded) and
 // the inverses of its 8x8 diagonal blocks are in shared memory.  Blocked by
 // 8 columns: R_b = S_b - X_<b * M_<b,b (DMMA), X_b = R_b * inv(M_bb) (DMMA).
-template <int NF>
+template <int NF, bool SMEM = false>
 __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long rs, long long cs,
                                           int nrows, int T, const double* __restrict__ Ms,
                                           const double* __restrict__ Minv) {
@@ -702,7 +551,8 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = b * 8 + 2 * t + h;
-        ra[b][mf][h] = (rv && c < T) ? __ldcg(row + static_cast<long long>(c) * cs) : 0.0;
+        const double* src = row + static_cast<long long>(c) * cs;
+        ra[b][mf][h] = (rv && c < T) ? (SMEM ? *src : __ldcg(src)) : 0.0;
       }
   }
   // source lanes of the accumulator -> A-fragment relayout inside a quad:
@@ -769,6 +619,166 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
   }
 }
 
+// ---------------------------------------------------------------- walker
+// CTA 0 walks the diagonal: per panel step k it applies the step-(k-1)
+// update to tile (k,k) with the L and U tiles it solved itself, factors the
+// tile, and solves the first tiles of the panel (L(k+1,k), U(k,k+1)), all in
+// shared memory — the latency-critical chain DIAG(k) -> TRSM -> GEMM ->
+// DIAG(k+1) never leaves the SM.  The other CTAs run the bulk TRSM/GEMM tasks
+// from the queue; the walker publishes its tiles with the same counters.
+template <int NF, bool CHOL>
+__device__ void walker(const Params& p, double* dsm) {
+  constexpr int Tp = NF * 8;
+  double* D = dsm;                          // tile (k,k)
+  double* Lt = dsm + kSmemB;                // tile (k+1,k): A21 -> L21
+  double* Ut = Lt + kSmemB;                 // tile (k,k+1): A12 -> U12 (LU)
+  double* Mu = Ut + kSmemB;                 // M of the L21 solve
+  double* Ml = Mu + kSmemB;                 // M of the U12 solve (LU)
+  double* rk = dsm + kSmemB + kSmemA + 9 * 64 + 2 * kPB;  // 128
+  double* inv = rk + 128;                   // 1024: DIAG block inverses
+  double* invX = inv + 1024;                // 512: inverses for the second solve
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int T = p.T, nt = p.nt;
+  const long long ld = p.ld;
+  __shared__ int s_ok;
+  auto wait1 = [&](const int* c, int need) -> bool {  // whole CTA
+    if (tid == 0) s_ok = wait_ge(p, c, need);
+    __syncthreads();
+    return s_ok;
+  };
+  auto stamp = [&](int k, int i) {
+    if (p.trace && tid == 0)
+      p.trace[8 * (static_cast<long long>(p.ntasks) + k) + i] = globaltimer();
+  };
+  for (int k = 0; k < nt; ++k) {
+    const int kT = k * T;
+    double* dk = p.a + static_cast<long long>(kT) * ld + kT;
+    stamp(k, 0);
+    // stages 0..k-2 of tile (k,k) come from the queue's GEMM tasks
+    if (k >= 2 && !wait1(&p.cnt[k * nt + k], (k - 1) * T)) return;
+    stamp(k, 1);
+    tile_load<CHOL>(D, dk, ld, T);
+    __syncthreads();
+    if (k >= 1) {  // stage k-1: D -= L(k,k-1) * U(k-1,k) (Cholesky: L L^T), DMMA in smem
+      if (8 * warp < Tp) {
+        const int r = 8 * warp;
+        double acc[NF][2];
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf) {
+          acc[nf][0] = D[(r + g) * kNP + nf * 8 + 2 * t];
+          acc[nf][1] = D[(r + g) * kNP + nf * 8 + 2 * t + 1];
+        }
+#pragma unroll
+        for (int s4 = 0; s4 < 2 * NF; ++s4) {
+          if (4 * s4 < T) {
+            const double a = -Lt[(r + g) * kNP + 4 * s4 + t];
+#pragma unroll
+            for (int nf = 0; nf < NF; ++nf) {
+              const double bv = CHOL ? Lt[(nf * 8 + g) * kNP + 4 * s4 + t]
+                                     : Ut[(4 * s4 + t) * kNP + nf * 8 + g];
+              dmma_8x8x4(acc[nf][0], acc[nf][1], a, bv);
+            }
+          }
+        }
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf) {
+          D[(r + g) * kNP + nf * 8 + 2 * t] = acc[nf][0];
+          D[(r + g) * kNP + nf * 8 + 2 * t + 1] = acc[nf][1];
+        }
+      }
+      __syncthreads();
+    }
+    stamp(k, 2);
+    diag_blocked<CHOL>(D, T, kT, p.info, inv, rk);
+    stamp(k, 3);
+    tile_store<CHOL>(D, dk, ld, T, rk, p.solve + static_cast<long long>(k) * kSolveSlot);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      if (diag::failed(p.info))
+        atomicExch(p.abort, 1);
+      else
+        red_release_add(&p.cnt[k * nt + k], k >= 1 ? 2 * T : T);  // stage k-1 + DIAG(k)
+    }
+    if (diag::failed(p.info)) return;
+    if (k + 1 >= nt) break;
+    // ---- first tiles of the panel: L(k+1,k) = A(k+1,k) U11^-1, U(k,k+1) = L11^-1 A(k,k+1)
+    if (!wait1(&p.cnt[(k + 1) * nt + k], kT)) return;
+    if (!CHOL && !wait1(&p.cnt[k * nt + k + 1], kT)) return;
+    stamp(k, 4);
+    {
+      const double* al = p.a + static_cast<long long>(kT + T) * ld + kT;
+      const double* au = dk + T;
+      constexpr int kPer = (Tp * Tp + kThreads - 1) / kThreads;
+      double vl[kPer], vu[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int e = tid + u * kThreads, x = e / Tp, y = e - x * Tp;
+        const bool in = e < Tp * Tp && x < T && y < T;
+        vl[u] = in ? __ldcg(al + static_cast<long long>(x) * ld + y) : 0.0;
+        vu[u] = (!CHOL && in) ? __ldcg(au + static_cast<long long>(x) * ld + y) : 0.0;
+      }
+      // M of the solves from the factored tile (diagonal never read)
+      for (int e = tid; e < Tp * Tp; e += kThreads) {
+        const int kk = e / Tp, c = e - kk * Tp;
+        const bool up = c > kk && c < T;
+        if (CHOL) {
+          Mu[kk * kNP + c] = up ? D[c * kNP + kk] * rk[64 + kk] : 0.0;  // L^T (scaled)
+        } else {
+          Mu[kk * kNP + c] = up ? D[kk * kNP + c] : 0.0;  // U11
+          Ml[kk * kNP + c] = up ? D[c * kNP + kk] : 0.0;  // L11^T (unit)
+        }
+      }
+      // block inverses of the second M: LU inv(L_bb^T) = inv(L_bb)^T;
+      // Cholesky inv(diag(l) L_bb^T) = inv(L_bb)^T diag(1/l)
+      for (int e = tid; e < NF * 64; e += kThreads) {
+        const int b = e >> 6, ii = (e >> 3) & 7, c = e & 7;
+        const double v = inv[512 + b * 64 + c * 8 + ii];
+        invX[e] = CHOL ? v * (8 * b + c < T ? rk[8 * b + c] : 1.0) : v;
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int e = tid + u * kThreads, x = e / Tp, y = e - x * Tp;
+        if (e < Tp * Tp) {
+          Lt[x * kNP + y] = vl[u];
+          if (!CHOL) Ut[x * kNP + y] = vu[u];
+        }
+      }
+    }
+    __syncthreads();
+    // warps 0..3: L21 strips (X * M = A21); warps 4..7: U12 strips on the
+    // transposed view (X * L11^T = A12^T)
+    {
+      const int sw = warp & 3;
+      const int c0 = sw * kStrip;
+      if (c0 < T) {
+        const int nr = min(kStrip, T - c0);
+        if (warp < 4)
+          warp_trsm<NF, true>(Lt + c0 * kNP, kNP, 1, nr, T, Mu, CHOL ? invX : inv);
+        else if (!CHOL)
+          warp_trsm<NF, true>(Ut + c0, 1, kNP, nr, T, Ml, invX);
+      }
+    }
+    __syncthreads();
+    {  // publish the solved tiles
+      double* gl = p.a + static_cast<long long>(kT + T) * ld + kT;
+      double* gu = dk + T;
+      for (int e = tid; e < T * T; e += kThreads) {
+        const int x = e / T, y = e - x * T;
+        gl[static_cast<long long>(x) * ld + y] = Lt[x * kNP + y];
+        if (!CHOL) gu[static_cast<long long>(x) * ld + y] = Ut[x * kNP + y];
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      red_release_add(&p.cnt[(k + 1) * nt + k], T);
+      if (!CHOL) red_release_add(&p.cnt[k * nt + k + 1], T);
+    }
+    stamp(k, 5);
+  }
+}
+
 // ---------------------------------------------------------------- kernel
 
 template <int NF, bool CHOL>
@@ -778,8 +788,6 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
   double* sm = dsm;                      // B (GEMM) / M (TRSM): Tp x kNP
   double* abuf = dsm + kSmemB;           // per-warp A strips
   double* minv = abuf + kSmemA;          // 8 x (8x8) block inverses + 64 diagonal reciprocals
-  double* pbuf = minv + 9 * 64;          // DIAG: 2 x kPB
-  double* rk = pbuf + 2 * kPB;           // DIAG: 128 per-column reciprocals / l_cc
   __shared__ int4 s_task[2];
   __shared__ int s_id[2];
   __shared__ int s_go;
@@ -792,6 +800,10 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
   const long long ld = p.ld;
   const int4 kNone = make_int4(-1, 0, 0, 0);
 
+  if (blockIdx.x == 0) {
+    walker<NF, CHOL>(p, dsm);
+    return;
+  }
   if (tid == 0) {
     const int id = atomicAdd(p.next, 1);
     s_id[0] = id;
@@ -827,18 +839,7 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
     stamp(1);
     stamp(2);
     stamp(3);
-    if (kind == kDiag) {
-      tile_factor_blocked<CHOL>(dk, ld, T, kT, p.info, sm, pbuf, rk, p.trace ? s_ph : nullptr,
-                                p.solve + static_cast<long long>(k) * kSolveSlot);
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) {
-        if (diag::failed(p.info))
-          atomicExch(p.abort, 1);
-        else
-          red_release_add(&p.cnt[k * nt + k], T);
-      }
-    } else if (kind == kGemm) {
+    if (kind == kGemm) {
       // B = U(k, j) (LU) or L(j, k)^T (Cholesky), zero-padded to Tp x Tp
       const double* bsrc = CHOL ? p.a + static_cast<long long>(j * T) * ld + kT
                                 : p.a + static_cast<long long>(kT) * ld + j * T;
@@ -976,12 +977,12 @@ cudaError_t launch_nf(int nf, const Params& prm, int grid, cudaStream_t s) {
 
 long long count_tasks(bool chol, int n, int by, int bx) {
   const int nt = n / bx;
-  long long total = 1;
+  long long total = 0;
   for (int k = 0; k + 1 < nt; ++k) {
     const int pe = (k + 1) * bx;
     const long long regions = (n - pe + by - 1) / by;
     const long long cols = nt - k - 1;
-    total += regions + 1 + (chol ? 0 : cols) + regions * cols;
+    total += regions + (chol ? 0 : cols) + regions * cols;
   }
   return total;
 }
@@ -993,34 +994,32 @@ bool eligible(int n, int by, int bx) {
   return count_tasks(false, n, by, bx) <= kMaxTasks;
 }
 
+// The walker CTA owns DIAG(k), L(k+1,k), U(k,k+1) and the update of the
+// diagonal tiles; the queue holds everything else, per step k: the L21 row
+// regions below tile row k+1, the U12 tiles right of column k+1, then the
+// trailing GEMM regions column by column (the columns the walker needs next
+// come first).  Row regions are `by` rows anchored at the panel end, the
+// reference's trailing tiling (kernels.cpp:205-216).
 std::vector<int4> build_tasks(bool chol, int n, int by, int bx) {
   const int T = bx, nt = n / bx;
   std::vector<int4> v;
   v.reserve(static_cast<size_t>(count_tasks(chol, n, by, bx)));
   auto task = [&](int kind, int k, int r0, int r1, int j) {
-    v.push_back(make_int4(kind | (j << 2), k, r0, r1));
+    if (r0 < r1) v.push_back(make_int4(kind | (j << 2), k, r0, r1));
   };
-  task(kDiag, 0, 0, T, 0);
   for (int k = 0; k + 1 < nt; ++k) {
     const int pe = (k + 1) * T;
     std::vector<std::pair<int, int>> reg;
     for (int r = pe; r < n; r += by) reg.emplace_back(r, std::min(n, r + by));
-    auto gemm = [&](size_t ri, int j) {
-      int r0 = reg[ri].first;
-      const int r1 = reg[ri].second;
-      if (chol) r0 = std::max(r0, j * T);  // lower triangle only
-      if (r0 < r1) task(kGemm, k, r0, r1, j);
-    };
-    // critical chain of step k -> DIAG(k+1): first solves, column k+1
-    task(kTrsmL, k, reg[0].first, reg[0].second, 0);
-    if (!chol) task(kTrsmU, k, 0, 0, k + 1);
-    for (size_t ri = 1; ri < reg.size(); ++ri) task(kTrsmL, k, reg[ri].first, reg[ri].second, 0);
-    for (size_t ri = 0; ri < reg.size(); ++ri) gemm(ri, k + 1);
-    task(kDiag, k + 1, 0, T, 0);  // look-ahead: overlaps the rest of step k
+    for (const auto& rg : reg) task(kTrsmL, k, std::max(rg.first, pe + T), rg.second, 0);
     if (!chol)
-      for (int j = k + 2; j < nt; ++j) task(kTrsmU, k, 0, 0, j);
-    for (int j = k + 2; j < nt; ++j)
-      for (size_t ri = 0; ri < reg.size(); ++ri) gemm(ri, j);
+      for (int j = k + 2; j < nt; ++j) task(kTrsmU, k, 0, 1, j);
+    for (int j = k + 1; j < nt; ++j)
+      for (const auto& rg : reg) {
+        int r0 = std::max(rg.first, chol ? j * T : pe);  // Cholesky: lower triangle only
+        if (j == k + 1) r0 = std::max(r0, pe + T);        // tile (k+1,k+1): the walker
+        task(kGemm, k, r0, rg.second, j);
+      }
   }
   return v;
 }
@@ -1029,6 +1028,7 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   const std::vector<int4> tasks = build_tasks(chol, n, by, bx);
   const int nt = n / bx;
   w->ntasks = static_cast<int>(tasks.size());
+  w->nsteps = n / bx;
   w->cnt_bytes = (static_cast<size_t>(nt) * nt + 2) * sizeof(int);
   cudaError_t e = cudaMalloc(&w->tasks, tasks.size() * sizeof(int4));
   if (e != cudaSuccess) return e;
@@ -1040,13 +1040,13 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   if (e != cudaSuccess) return e;
   const char* tr = std::getenv("TT_DAG_TRACE");
   if (tr && tr[0] == '1') {
-    e = cudaMalloc(&w->trace, tasks.size() * 8 * sizeof(unsigned long long));
+    e = cudaMalloc(&w->trace, (tasks.size() + nt) * 8 * sizeof(unsigned long long));
     if (e != cudaSuccess) return e;
   }
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  w->grid = std::max(1, std::min(sms, w->ntasks));
+  w->grid = 1 + std::max(0, std::min(sms - 1, w->ntasks));  // walker + queue workers
   return cudaSuccess;
 }
 

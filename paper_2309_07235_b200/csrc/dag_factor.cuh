@@ -49,6 +49,7 @@ std::vector<int4> build_tasks(bool chol, int n, int by, int bx);
 struct Workspace {
   int4* tasks = nullptr;   // device task list
   int ntasks = 0;
+  int nsteps = 0;          // n / bx: walker steps (trace rows after the tasks)
   int* cnt = nullptr;      // nt*nt tile counters + 1 task counter + 1 abort flag
   size_t cnt_bytes = 0;
   int grid = 0;

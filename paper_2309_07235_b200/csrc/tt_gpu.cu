@@ -877,12 +877,13 @@ int tt_dag_trace(tt_ctx* ctx, unsigned long long* out, int cap) {
   if (!ctx || !ctx->dag_last || !ctx->dag_last->trace) return -1;
   const tt::dag::Workspace* w = ctx->dag_last;
   TT_CUDA(ctx, cudaStreamSynchronize(ctx->stream), "trace sync");
-  const int m = std::min(w->ntasks, std::max(cap, 0));
+  const int total = w->ntasks + w->nsteps;  // queue tasks, then one row per walker step
+  const int m = std::min(total, std::max(cap, 0));
   if (out && m > 0)
     TT_CUDA(ctx, cudaMemcpy(out, w->trace, static_cast<size_t>(m) * 8 * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost),
             "trace copy");
-  return w->ntasks;
+  return total;
 }
 
 int tt_dev_gemm(tt_ctx* ctx, const double* a, int lda, const double* b, int ldb, int b_trans,

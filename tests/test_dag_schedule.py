@@ -1,10 +1,14 @@
 """Host-side checks of the persistent tile-DAG schedule (dag_factor.cu), no GPU.
 
-The task list is built by the C++ library (tt_dag_tasks).  These tests prove,
-for LU and Cholesky over ragged knob combinations, that
-  * list order is a valid execution order under the kernel's counter protocol
-    (every task's wait condition already holds when it is reached, so the
-    persistent kernel, which takes tasks in list order, cannot deadlock);
+The queue's task list is built by the C++ library (tt_dag_tasks); the walker
+CTA's per-step work (update + DIAG of tile (k,k), L(k+1,k), U(k,k+1)) is
+modelled here exactly as the kernel runs it.  These tests prove, for LU and
+Cholesky over ragged knob combinations, that
+  * running walker step k before the first queue task of step k is a valid
+    execution order under the kernel's counter protocol (every wait
+    condition already holds when it is reached; the queue is taken in list
+    order and only waits on earlier tasks or earlier walker steps, so the
+    persistent kernel cannot deadlock);
   * every tile receives each of its stages exactly once and ends complete;
   * executing the tasks in list order with plain numpy arithmetic reproduces
     the reference factorisation (oracle), i.e. the task decomposition
@@ -56,25 +60,63 @@ def signals(kind, j, k, r0, r1, T):
     return {(i, col): min(r1, (i + 1) * T) - max(r0, i * T) for i in tiles(r0, r1, T)}
 
 
+def walker_needs(k, T, nt, chol):
+    out = []
+    if k >= 2:
+        out.append(((k, k), (k - 1) * T))
+    if k + 1 < nt:
+        out.append(((k + 1, k), k * T))
+        if not chol:
+            out.append(((k, k + 1), k * T))
+    return out
+
+
+def walker_signals(k, T, nt, chol):
+    sig = {(k, k): 2 * T if k >= 1 else T}
+    if k + 1 < nt:
+        sig[(k + 1, k)] = T
+        if not chol:
+            sig[(k, k + 1)] = T
+    return sig
+
+
+def interleaved(tasks, nt):
+    """Queue tasks with walker step k inserted before the first task of step k."""
+    out, nextw = [], 0
+    for t in tasks:
+        k = int(t[1])
+        while nextw <= k:
+            out.append(("W", nextw))
+            nextw += 1
+        out.append(("Q", t))
+    while nextw < nt:
+        out.append(("W", nextw))
+        nextw += 1
+    return out
+
+
 @pytest.mark.parametrize("kernel,n,by,bx", CASES)
 def test_task_order_and_coverage(kernel, n, by, bx):
     tasks = _lib.dag_tasks(kernel, n, by, bx)
     assert tasks is not None
     chol = kernel == "cholesky"
     T, nt = bx, n // bx
+    assert not np.any((tasks[:, 0] & 3) == DIAG)  # DIAG belongs to the walker
     cnt = np.zeros((nt, nt), dtype=np.int64)
-    for t in tasks:
-        kind, j, k, r0, r1 = decode(t)
-        for (tile, need) in needs(kind, j, k, r0, r1, T, chol):
-            assert cnt[tile] >= need, (t, tile, need, cnt[tile])
-        for tile, rows in signals(kind, j, k, r0, r1, T).items():
+    for what, t in interleaved(tasks, nt):
+        if what == "W":
+            need, sig = walker_needs(t, T, nt, chol), walker_signals(t, T, nt, chol)
+        else:
+            kind, j, k, r0, r1 = decode(t)
+            need, sig = needs(kind, j, k, r0, r1, T, chol), signals(kind, j, k, r0, r1, T)
+        for (tile, nd) in need:
+            assert cnt[tile] >= nd, (what, t, tile, nd, cnt[tile])
+        for tile, rows in sig.items():
             i, jj = tile
             if chol:
                 assert i >= jj, t
-            stage = k if kind == GEMM else min(i, jj)
-            # the rows land in this tile's current stage
-            assert stage * T <= cnt[tile] and cnt[tile] + rows <= (stage + 1) * T, (t, tile)
             cnt[tile] += rows
+            assert cnt[tile] <= (min(i, jj) + 1) * T, (what, t, tile)
     for i in range(nt):
         for jj in range(nt):
             if chol and jj > i:
@@ -86,32 +128,54 @@ def test_task_order_and_coverage(kernel, n, by, bx):
 def run_tasks_numpy(a, tasks, bx, chol):
     a = a.copy()
     T = bx
-    for t in tasks:
-        kind, j, k, r0, r1 = decode(t)
-        kT, jT = k * T, j * T
+    nt = a.shape[0] // T
+
+    def trsm_l(k, r0, r1):
+        kT = k * T
         d = a[kT:kT + T, kT:kT + T]
-        if kind == DIAG:
-            blk = d.copy()
+        m = np.tril(d).T if chol else np.triu(d)
+        a[r0:r1, kT:kT + T] = np.linalg.solve(m.T, a[r0:r1, kT:kT + T].T).T
+
+    def trsm_u(k, j):
+        kT, jT = k * T, j * T
+        lo = np.tril(a[kT:kT + T, kT:kT + T], -1) + np.eye(T)
+        a[kT:kT + T, jT:jT + T] = np.linalg.solve(lo, a[kT:kT + T, jT:jT + T])
+
+    def gemm(k, r0, r1, j):
+        kT, jT = k * T, j * T
+        b = a[jT:jT + T, kT:kT + T].T if chol else a[kT:kT + T, jT:jT + T]
+        upd = a[r0:r1, jT:jT + T] - a[r0:r1, kT:kT + T] @ b
+        if chol:
+            rows = np.arange(r0, r1)[:, None]
+            cols = np.arange(jT, jT + T)[None, :]
+            upd = np.where(rows >= cols, upd, a[r0:r1, jT:jT + T])
+        a[r0:r1, jT:jT + T] = upd
+
+    for what, t in interleaved(tasks, nt):
+        if what == "W":  # walker step k
+            k = t
+            kT = k * T
+            if k >= 1:
+                gemm(k - 1, kT, kT + T, k)
+            blk = a[kT:kT + T, kT:kT + T].copy()
             if chol:
                 oracle.cholesky_factor_inplace(blk, T, T)
                 a[kT:kT + T, kT:kT + T][np.tril_indices(T)] = blk[np.tril_indices(T)]
             else:
                 oracle.lu_factor_inplace(blk, T, T)
                 a[kT:kT + T, kT:kT + T] = blk
-        elif kind == TRSM_L:
-            m = np.tril(d).T if chol else np.triu(d)
-            a[r0:r1, kT:kT + T] = np.linalg.solve(m.T, a[r0:r1, kT:kT + T].T).T
+            if k + 1 < nt:
+                trsm_l(k, kT + T, kT + 2 * T)
+                if not chol:
+                    trsm_u(k, k + 1)
+            continue
+        kind, j, k, r0, r1 = decode(t)
+        if kind == TRSM_L:
+            trsm_l(k, r0, r1)
         elif kind == TRSM_U:
-            lo = np.tril(d, -1) + np.eye(T)
-            a[kT:kT + T, jT:jT + T] = np.linalg.solve(lo, a[kT:kT + T, jT:jT + T])
+            trsm_u(k, j)
         else:
-            b = a[jT:jT + T, kT:kT + T].T if chol else a[kT:kT + T, jT:jT + T]
-            upd = a[r0:r1, jT:jT + T] - a[r0:r1, kT:kT + T] @ b
-            if chol:
-                rows = np.arange(r0, r1)[:, None]
-                cols = np.arange(jT, jT + T)[None, :]
-                upd = np.where(rows >= cols, upd, a[r0:r1, jT:jT + T])
-            a[r0:r1, jT:jT + T] = upd
+            gemm(k, r0, r1, j)
     return a
 
 

@@ -21,15 +21,17 @@ for _ in range(3):
     r.run((by, bx), want_output=False)
 tasks = _lib.dag_tasks(kern, n, by, bx)
 nt = len(tasks)
-tr = np.zeros((nt, 8), dtype=np.uint64)
-got = ctx.lib.tt_dag_trace(ctx.handle, tr.ctypes.data_as(ctypes.c_void_p), nt)
-assert got == nt, got
+nsteps = n // bx
+trall = np.zeros((nt + nsteps, 8), dtype=np.uint64)
+got = ctx.lib.tt_dag_trace(ctx.handle, trall.ctypes.data_as(ctypes.c_void_p), nt + nsteps)
+tr = trall[:nt]
+wk = (trall[nt:, :6].astype(np.int64) - int(tr[:, 0].min())) / 1e3
 t = tr[:, :3].astype(np.int64)
 t0 = t[:, 0].min()
 t = (t - t0) / 1e3  # us
 kind = tasks[:, 0] & 3
 names = ["DIAG", "TRSM_L", "TRSM_U", "GEMM"]
-span = t[:, 2].max()
+span = max(t[:, 2].max(), wk[:, 5].max())
 print(f"{kern} n={n} ({by},{bx}): {nt} tasks, span {span:.1f} us, SMs used {len(set(tr[:, 3]))}")
 for k in range(4):
     m = kind == k
@@ -38,10 +40,11 @@ for k in range(4):
         wait = t[m, 1] - t[m, 0]
         print(f"  {names[k]:6s} n={m.sum():6d} run mean {run.mean():7.2f} max {run.max():7.2f} "
               f"| wait mean {wait.mean():7.2f} max {wait.max():7.2f} us | busy sum {run.sum():9.1f}")
-dm = kind == 0
-ph = (tr[dm, 4:6].astype(np.int64) - t0) / 1e3
-print("  DIAG phases (us after ready): load+sync %.2f, loop %.2f, rest %.2f" % (
-    (ph[:, 0] - t[dm, 1]).mean(), (ph[:, 1] - ph[:, 0]).mean(), (t[dm, 2] - ph[:, 1]).mean()))
+w = wk[1:-1]
+print("  walker per step (us): wait tile %.2f, update %.2f, DIAG %.2f, store+wait panel %.2f, L/U tiles %.2f | period %.2f" % (
+    (w[:, 1] - w[:, 0]).mean(), (w[:, 2] - w[:, 1]).mean(), (w[:, 3] - w[:, 2]).mean(),
+    (w[:, 4] - w[:, 3]).mean(), (w[:, 5] - w[:, 4]).mean(), np.diff(wk[:, 0]).mean()))
+print("  walker step k=5: " + " ".join("%.1f" % x for x in wk[5]))
 for kk, nm, a_, b_ in [(2, "TRSM_U", "M load+sync", "8x8 inverses+sync"), (1, "TRSM_L", "M load+sync", "8x8 inverses+sync"), (3, "GEMM", "B load+sync", "first strip (warp 0) done")]:
     mm = kind == kk
     if mm.any():
@@ -54,11 +57,6 @@ print("  GEMM first strip (warp 0): data ready +%.2f, computed+stored +%.2f, fen
 busy = (t[:, 2] - t[:, 1]).sum()
 grid = len(set(tr[:, 3]))
 print(f"  utilisation (task run time / (SMs x span)) = {busy / (grid * span):.3f}")
-d = np.where(kind == 0)[0]
-print("  DIAG chain (k: ready, done, gap since previous DIAG done):")
-prev = 0.0
-for i, idx in enumerate(d[:8].tolist() + d[-3:].tolist()):
-    print(f"    k={tasks[idx, 1]:4d} ready {t[idx, 1]:8.1f} done {t[idx, 2]:8.1f} gap {t[idx, 1] - prev:7.1f}")
-    prev = t[idx, 2]
+
 if len(sys.argv) > 5:
     np.savez(sys.argv[5], tasks=tasks, trace=tr)

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout -s KILL 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; tail -c 2500 gpurun_out/bench.json; tail -3 gpurun_out/bench.err
+timeout -s KILL 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_lu_dag.csv python tools/one_run.py --kernel lu --dims 2000 --cfg 400,50 --runs 2 > gpurun_out/ncu_launch.log 2>&1; echo "ncu launch rc=$?"
+timeout -s KILL 400 ncu --set full --clock-control none --import-source on -k regex:"dag_kernel" -s 1 -c 1 -o gpurun_out/prof_dag_lu2000_v4 python tools/one_run.py --kernel lu --dims 2000 --cfg 400,50 --runs 2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
