@@ -16,6 +16,7 @@
 // Per element the arithmetic is fixed by the task list, independent of
 // which CTA runs a task or when: repeated runs are bitwise identical
 // (kernels_test.cpp:284-296).
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 
@@ -980,7 +981,7 @@ long long count_tasks(bool chol, int n, int by, int bx) {
   long long total = 0;
   for (int k = 0; k + 1 < nt; ++k) {
     const int pe = (k + 1) * bx;
-    const long long regions = (n - pe + by - 1) / by;
+    const long long regions = (n - 1) / by - pe / by + 1;
     const long long cols = nt - k - 1;
     total += regions + (chol ? 0 : cols) + regions * cols;
   }
@@ -995,33 +996,54 @@ bool eligible(int n, int by, int bx) {
 }
 
 // The walker CTA owns DIAG(k), L(k+1,k), U(k,k+1) and the update of the
-// diagonal tiles; the queue holds everything else, per step k: the L21 row
-// regions below tile row k+1, the U12 tiles right of column k+1, then the
-// trailing GEMM regions column by column (the columns the walker needs next
-// come first).  Row regions are `by` rows anchored at the panel end, the
-// reference's trailing tiling (kernels.cpp:205-216).
+// diagonal tiles; the queue holds everything else: per step k the L21 row
+// regions below tile row k+1, the U12 tiles right of column k+1, and the
+// trailing GEMM regions.  Row regions are `by` rows (the reference's
+// trailing row tile, kernels.cpp:205-216) aligned to multiples of by and
+// clipped to the trailing rows, so a region's tiles are updated by the same
+// region task at every step.
+//
+// Order: step by step (every task of step k depends only on walker step k
+// and on step k-1 tasks, so the queue never waits on a task behind it, and
+// walker step k+1 needs only step-k tasks and walker step k: no deadlock).
+// Inside a step the tasks the walker needs next come first — the L21
+// regions, U(k,k+2), the GEMM regions of tiles (k+2,k+1), (k+1,k+2),
+// (k+2,k+2) — then the rest, column by column.
 std::vector<int4> build_tasks(bool chol, int n, int by, int bx) {
   const int T = bx, nt = n / bx;
-  std::vector<int4> v;
-  v.reserve(static_cast<size_t>(count_tasks(chol, n, by, bx)));
-  auto task = [&](int kind, int k, int r0, int r1, int j) {
-    if (r0 < r1) v.push_back(make_int4(kind | (j << 2), k, r0, r1));
-  };
+  std::vector<int4> out;
+  out.reserve(static_cast<size_t>(count_tasks(chol, n, by, bx)));
+  std::vector<char> done;
   for (int k = 0; k + 1 < nt; ++k) {
     const int pe = (k + 1) * T;
-    std::vector<std::pair<int, int>> reg;
-    for (int r = pe; r < n; r += by) reg.emplace_back(r, std::min(n, r + by));
-    for (const auto& rg : reg) task(kTrsmL, k, std::max(rg.first, pe + T), rg.second, 0);
+    std::vector<int4> step;
+    auto task = [&](int kind, int r0, int r1, int j) {
+      if (r0 < r1) step.push_back(make_int4(kind | (j << 2), k, r0, r1));
+    };
+    std::vector<std::pair<int, int>> reg;  // row regions: multiples of by, clipped
+    for (int r = (pe / by) * by; r < n; r += by) reg.emplace_back(std::max(r, pe), std::min(n, r + by));
+    for (const auto& rg : reg) task(kTrsmL, std::max(rg.first, pe + T), rg.second, 0);  // row k+1: walker
     if (!chol)
-      for (int j = k + 2; j < nt; ++j) task(kTrsmU, k, 0, 1, j);
+      for (int j = k + 2; j < nt; ++j) task(kTrsmU, 0, 1, j);
     for (int j = k + 1; j < nt; ++j)
       for (const auto& rg : reg) {
         int r0 = std::max(rg.first, chol ? j * T : pe);  // Cholesky: lower triangle only
         if (j == k + 1) r0 = std::max(r0, pe + T);        // tile (k+1,k+1): the walker
-        task(kGemm, k, r0, rg.second, j);
+        task(kGemm, r0, rg.second, j);
       }
+    // urgent first (stable): all L21 regions (any GEMM region may straddle
+    // into them), U(k,k+2), and the GEMM regions touching tile rows <= k+2
+    // in columns <= k+2
+    auto urgent = [&](const int4& t) {
+      const int kind = t.x & 3, j = t.x >> 2;
+      if (kind == kTrsmU) return j == k + 2;
+      if (kind == kTrsmL) return true;
+      return j <= k + 2 && t.z / T <= k + 2;
+    };
+    std::stable_partition(step.begin(), step.end(), urgent);
+    out.insert(out.end(), step.begin(), step.end());
   }
-  return v;
+  return out;
 }
 
 cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {

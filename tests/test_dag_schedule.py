@@ -80,18 +80,35 @@ def walker_signals(k, T, nt, chol):
     return sig
 
 
-def interleaved(tasks, nt):
-    """Queue tasks with walker step k inserted before the first task of step k."""
-    out, nextw = [], 0
+def interleaved(tasks, nt, T, chol):
+    """The kernel's semantics sequentialised: the walker runs each step as soon
+    as its dependencies hold; the queue is taken strictly in list order.  A
+    queue task whose wait condition does not hold when it is reached (with
+    the walker stuck) would deadlock the persistent kernel."""
+    cnt = np.zeros((nt, nt), dtype=np.int64)
+    out, s = [], 0
+
+    def walker_ready(s):
+        return all(cnt[tile] >= nd for tile, nd in walker_needs(s, T, nt, chol))
+
+    def run_walker():
+        nonlocal s
+        while s < nt and walker_ready(s):
+            out.append(("W", s))
+            for tile, rows in walker_signals(s, T, nt, chol).items():
+                cnt[tile] += rows
+            s += 1
+
     for t in tasks:
-        k = int(t[1])
-        while nextw <= k:
-            out.append(("W", nextw))
-            nextw += 1
+        run_walker()
+        kind, j, k, r0, r1 = decode(t)
+        for tile, nd in needs(kind, j, k, r0, r1, T, chol):
+            assert cnt[tile] >= nd, ("deadlock", t, tile, nd, cnt[tile], "walker at", s)
         out.append(("Q", t))
-    while nextw < nt:
-        out.append(("W", nextw))
-        nextw += 1
+        for tile, rows in signals(kind, j, k, r0, r1, T).items():
+            cnt[tile] += rows
+    run_walker()
+    assert s == nt, ("walker stuck at", s)
     return out
 
 
@@ -103,7 +120,7 @@ def test_task_order_and_coverage(kernel, n, by, bx):
     T, nt = bx, n // bx
     assert not np.any((tasks[:, 0] & 3) == DIAG)  # DIAG belongs to the walker
     cnt = np.zeros((nt, nt), dtype=np.int64)
-    for what, t in interleaved(tasks, nt):
+    for what, t in interleaved(tasks, nt, T, chol):
         if what == "W":
             need, sig = walker_needs(t, T, nt, chol), walker_signals(t, T, nt, chol)
         else:
@@ -151,7 +168,7 @@ def run_tasks_numpy(a, tasks, bx, chol):
             upd = np.where(rows >= cols, upd, a[r0:r1, jT:jT + T])
         a[r0:r1, jT:jT + T] = upd
 
-    for what, t in interleaved(tasks, nt):
+    for what, t in interleaved(tasks, nt, T, chol):
         if what == "W":  # walker step k
             k = t
             kT = k * T
