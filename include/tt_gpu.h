@@ -144,6 +144,9 @@ int tt_dev_fill_uniform(tt_ctx* ctx, double* a, int rows, int cols, int ld, long
  * -1 when (n, by, bx) runs on the launch-per-kernel graph schedule instead.
  * Needs no device. */
 int tt_dag_tasks(int kernel, int n, int by, int bx, int* out, int cap);
+/* Number of leading tasks of that list forming the urgent queue (the rest is
+ * the bulk queue); -1 when the graph schedule runs instead. */
+int tt_dag_urgent(int kernel, int n, int by, int bx);
 
 /* With TT_DAG_TRACE=1 in the environment the persistent schedule records,
  * per task, {fetch, dependencies-ready, done} (%globaltimer ns) and the SM

@@ -26,7 +26,7 @@ EXPORTS = (
     "tt_setup_host", "tt_setup_seeded", "tt_run", "tt_measure", "tt_measure_samples",
     "tt_get_input", "tt_residual", "tt_dev_lu", "tt_dev_cholesky", "tt_dev_mm3",
     "tt_dev_gemm", "tt_dev_fill_uniform", "tt_launch_count", "tt_build_info", "tt_dag_tasks",
-    "tt_dag_trace",
+    "tt_dag_trace", "tt_dag_urgent",
 )
 
 _lib = None
@@ -72,6 +72,7 @@ def load() -> ctypes.CDLL:
         "tt_build_info": (ctypes.c_char_p, []),
         "tt_dag_tasks": (c_int, [c_int, c_int, c_int, c_int, c_int_p, c_int]),
         "tt_dag_trace": (c_int, [vp, vp, c_int]),
+        "tt_dag_urgent": (c_int, [c_int, c_int, c_int, c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -73,6 +73,8 @@ struct Params {
   int* info;
   unsigned long long* trace;  // optional: per task {fetch, ready, done ns, smid, 4 phase stamps}
   double* solve;  // per step: 64 reciprocals of the factored diagonal (DIAG -> TRSM)
+  int nurgent;    // tasks[0, nurgent): urgent queue; [nurgent, ntasks): bulk queue
+  int nuw;        // CTAs 1..nuw serve the urgent queue
 };
 
 
@@ -376,80 +378,119 @@ __device__ __forceinline__ void tile_load(double* D, const double* __restrict__ 
   }
 }
 
+// 8x8 diagonal block b (one warp, fragment layout, shuffles) + inv(U_bb),
+// inv(L_bb).  Called by warp 0 only.
+template <bool CHOL>
+__device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* info, double* inv,
+                                              double* rk, int b) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int p = 8 * b;
+  double* invU = inv + b * 64;
+  double* invL = inv + 512 + b * 64;
+  __syncwarp();  // converged warp: keeps the shuffles on the fast path
+  double v0 = D[(p + g) * kNP + p + 2 * t], v1 = D[(p + g) * kNP + p + 2 * t + 1];
+  double rr[8], pv[8];
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const double sel = (kk & 1) ? v1 : v0;
+    const double piv = __shfl_sync(0xffffffffu, sel, kk * 4 + (kk >> 1));
+    const double agk = __shfl_sync(0xffffffffu, sel, g * 4 + (kk >> 1));
+    const double u0 = __shfl_sync(0xffffffffu, v0, kk * 4 + t);
+    const double u1 = __shfl_sync(0xffffffffu, v1, kk * 4 + t);
+    const double r = rcp_nr(piv);
+    const double m = g > kk ? agk * r : 0.0;
+    if (2 * t > kk) v0 = fma(-m, u0, v0);
+    if (2 * t + 1 > kk) v1 = fma(-m, u1, v1);
+    if (g > kk && 2 * t == kk) v0 = m;
+    if (g > kk && 2 * t + 1 == kk) v1 = m;
+    rr[kk] = r;
+    pv[kk] = piv;
+  }
+  D[(p + g) * kNP + p + 2 * t] = v0;
+  D[(p + g) * kNP + p + 2 * t + 1] = v1;
+  // reciprocals and the reference's failure predicates, off the pivot chain
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    if (lane == kk && p + kk < T) {
+      rk[p + kk] = rr[kk];
+      const double piv = pv[kk];
+      if (CHOL ? piv <= 0.0 : fabs(piv) < 1e-300)
+        atomicMin(info, gcol + p + kk);  // kernels.cpp:187-190 / :297-302 (NaN passes)
+    }
+  }
+  __syncwarp();
+  // inv(U_bb): lanes 0..7 (column c, back substitution); inv(L_bb) (unit
+  // lower): lanes 8..15 (column c, forward substitution)
+  if (lane < 16) {
+    const int c = lane & 7;
+    double x[8];
+    if (lane < 8) {
+#pragma unroll
+      for (int ii = 7; ii >= 0; --ii) {
+        double acc = ii == c ? 1.0 : 0.0;
+#pragma unroll
+        for (int mm = ii + 1; mm < 8; ++mm) acc = fma(-D[(p + ii) * kNP + p + mm], x[mm], acc);
+        x[ii] = acc * (p + ii < T ? rk[p + ii] : 1.0);
+      }
+#pragma unroll
+      for (int ii = 0; ii < 8; ++ii) invU[ii * 8 + c] = x[ii];
+    } else {
+#pragma unroll
+      for (int ii = 0; ii < 8; ++ii) {
+        double acc = ii == c ? 1.0 : 0.0;
+#pragma unroll
+        for (int mm = 0; mm < ii; ++mm) acc = fma(-D[(p + ii) * kNP + p + mm], x[mm], acc);
+        x[ii] = acc;
+      }
+#pragma unroll
+      for (int ii = 0; ii < 8; ++ii) invL[ii * 8 + c] = x[ii];
+    }
+  }
+}
+
+// One warp: trailing update of block row ir (of step b) over block columns
+// jr in [jlo, nr): block (b+1+ir, b+1+jr) -= L(b+1+ir, b) * U(b, b+1+jr).
+__device__ __forceinline__ void trail_row(double* D, int b, int nr, int ir, int jlo) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int p = 8 * b, ib = 8 * (b + 1 + ir);
+  const double a0 = -D[(ib + g) * kNP + p + t], a1 = -D[(ib + g) * kNP + p + 4 + t];
+  double c0[7], c1[7];
+#pragma unroll
+  for (int jr = 0; jr < 7; ++jr) {
+    if (jr >= jlo && jr < nr) {
+      const int jb = 8 * (b + 1 + jr);
+      c0[jr] = D[(ib + g) * kNP + jb + 2 * t];
+      c1[jr] = D[(ib + g) * kNP + jb + 2 * t + 1];
+      const double b0 = D[(p + t) * kNP + jb + g], b1 = D[(p + 4 + t) * kNP + jb + g];
+      dmma_8x8x4(c0[jr], c1[jr], a0, b0);
+      dmma_8x8x4(c0[jr], c1[jr], a1, b1);
+    }
+  }
+#pragma unroll
+  for (int jr = 0; jr < 7; ++jr) {
+    if (jr >= jlo && jr < nr) {
+      const int jb = 8 * (b + 1 + jr);
+      D[(ib + g) * kNP + jb + 2 * t] = c0[jr];
+      D[(ib + g) * kNP + jb + 2 * t + 1] = c1[jr];
+    }
+  }
+}
+
+// Blocked elimination of the tile in shared memory with look-ahead: while
+// warps 1..7 apply step b's trailing update, warp 0 updates the next
+// diagonal block first and factors it, so the serial 8x8 chain of block b+1
+// overlaps the bulk of step b.  Two __syncthreads per 8 pivots.
 template <bool CHOL>
 __device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* info, double* inv,
                                              double* rk) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int NB = (T + 7) >> 3;
-  for (int b = 0; b < NB; ++b) {
-    const int p = 8 * b;
-    double* invU = inv + b * 64;
-    double* invL = inv + 512 + b * 64;
-    if (warp == 0) {
-      __syncwarp();  // converged warp: keeps the shuffles on the fast path
-      // ---- 8x8 diagonal block, lane (g,t) holds (g, 2t), (g, 2t+1)
-      double v0 = D[(p + g) * kNP + p + 2 * t], v1 = D[(p + g) * kNP + p + 2 * t + 1];
-      double rr[8], pv[8];
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const double sel = (kk & 1) ? v1 : v0;
-        const double piv = __shfl_sync(0xffffffffu, sel, kk * 4 + (kk >> 1));
-        const double agk = __shfl_sync(0xffffffffu, sel, g * 4 + (kk >> 1));
-        const double u0 = __shfl_sync(0xffffffffu, v0, kk * 4 + t);
-        const double u1 = __shfl_sync(0xffffffffu, v1, kk * 4 + t);
-        const double r = rcp_nr(piv);
-        const double m = g > kk ? agk * r : 0.0;
-        if (2 * t > kk) v0 = fma(-m, u0, v0);
-        if (2 * t + 1 > kk) v1 = fma(-m, u1, v1);
-        if (g > kk && 2 * t == kk) v0 = m;
-        if (g > kk && 2 * t + 1 == kk) v1 = m;
-        rr[kk] = r;
-        pv[kk] = piv;
-      }
-      D[(p + g) * kNP + p + 2 * t] = v0;
-      D[(p + g) * kNP + p + 2 * t + 1] = v1;
-      // reciprocals and the reference's failure predicates, off the pivot chain
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        if (lane == kk && p + kk < T) {
-          rk[p + kk] = rr[kk];
-          const double piv = pv[kk];
-          if (CHOL ? piv <= 0.0 : fabs(piv) < 1e-300)
-            atomicMin(info, gcol + p + kk);  // kernels.cpp:187-190 / :297-302 (NaN passes)
-        }
-      }
-      __syncwarp();
-      // inv(U_bb): lanes 0..7 (column c, back substitution); inv(L_bb) (unit
-      // lower): lanes 8..15 (column c, forward substitution)
-      if (lane < 16) {
-        const int c = lane & 7;
-        double x[8];
-        if (lane < 8) {
-#pragma unroll
-          for (int ii = 7; ii >= 0; --ii) {
-            double acc = ii == c ? 1.0 : 0.0;
-#pragma unroll
-            for (int mm = ii + 1; mm < 8; ++mm) acc = fma(-D[(p + ii) * kNP + p + mm], x[mm], acc);
-            x[ii] = acc * (p + ii < T ? rk[p + ii] : 1.0);
-          }
-#pragma unroll
-          for (int ii = 0; ii < 8; ++ii) invU[ii * 8 + c] = x[ii];
-        } else {
-#pragma unroll
-          for (int ii = 0; ii < 8; ++ii) {
-            double acc = ii == c ? 1.0 : 0.0;
-#pragma unroll
-            for (int mm = 0; mm < ii; ++mm) acc = fma(-D[(p + ii) * kNP + p + mm], x[mm], acc);
-            x[ii] = acc;
-          }
-#pragma unroll
-          for (int ii = 0; ii < 8; ++ii) invL[ii * 8 + c] = x[ii];
-        }
-      }
-    }
-    __syncthreads();
-    const int nr = NB - b - 1;  // blocks beyond the diagonal one
-    if (nr == 0) break;
+  if (warp == 0) factor_block8<CHOL>(D, T, gcol, info, inv, rk, 0);
+  __syncthreads();
+  for (int b = 0; b + 1 < NB; ++b) {
+    const int p = 8 * b, nr = NB - b - 1;
+    const double* invU = inv + b * 64;
+    const double* invL = inv + 512 + b * 64;
     // ---- panels: job < nr: L block (b+1+job, b) = A * inv(U_bb);
     //               job >= nr: U block (b, b+1+job-nr) = inv(L_bb) * A
     for (int job = warp; job < 2 * nr; job += kWarps) {
@@ -475,31 +516,12 @@ __device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* in
       }
     }
     __syncthreads();
-    // ---- trailing update: block (ib, jb) -= L(ib, b) * U(b, jb); warp w
-    // owns block row b+1+w (A fragments loaded once, all jb loads in flight)
-    for (int ir = warp; ir < nr; ir += kWarps) {
-      const int ib = 8 * (b + 1 + ir);
-      const double a0 = -D[(ib + g) * kNP + p + t], a1 = -D[(ib + g) * kNP + p + 4 + t];
-      double c0[7], c1[7];
-#pragma unroll
-      for (int jr = 0; jr < 7; ++jr) {
-        if (jr < nr) {
-          const int jb = 8 * (b + 1 + jr);
-          c0[jr] = D[(ib + g) * kNP + jb + 2 * t];
-          c1[jr] = D[(ib + g) * kNP + jb + 2 * t + 1];
-          const double b0 = D[(p + t) * kNP + jb + g], b1 = D[(p + 4 + t) * kNP + jb + g];
-          dmma_8x8x4(c0[jr], c1[jr], a0, b0);
-          dmma_8x8x4(c0[jr], c1[jr], a1, b1);
-        }
-      }
-#pragma unroll
-      for (int jr = 0; jr < 7; ++jr) {
-        if (jr < nr) {
-          const int jb = 8 * (b + 1 + jr);
-          D[(ib + g) * kNP + jb + 2 * t] = c0[jr];
-          D[(ib + g) * kNP + jb + 2 * t + 1] = c1[jr];
-        }
-      }
+    if (warp == 0) {  // look-ahead: diagonal block (b+1,b+1) first, then factor it
+      trail_row(D, b, 1, 0, 0);
+      __syncwarp();
+      factor_block8<CHOL>(D, T, gcol, info, inv, rk, b + 1);
+    } else {  // the rest of step b's trailing update
+      for (int ir = warp - 1; ir < nr; ir += kWarps - 1) trail_row(D, b, nr, ir, ir == 0 ? 1 : 0);
     }
     __syncthreads();
   }
@@ -805,10 +827,14 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
     walker<NF, CHOL>(p, dsm);
     return;
   }
+  // queue of this CTA: [qlo, qhi) of the task array, its own counter
+  const bool urgent_q = blockIdx.x <= p.nuw;
+  const int qlo = urgent_q ? 0 : p.nurgent, qhi = urgent_q ? p.nurgent : p.ntasks;
+  int* qnext = urgent_q ? p.next : p.next + 2;
   if (tid == 0) {
-    const int id = atomicAdd(p.next, 1);
+    const int id = qlo + atomicAdd(qnext, 1);
     s_id[0] = id;
-    s_task[0] = id < p.ntasks ? p.tasks[id] : kNone;
+    s_task[0] = id < qhi ? p.tasks[id] : kNone;
   }
   __syncthreads();
   for (int it = 0;; ++it) {
@@ -819,14 +845,14 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
       int nid = 0;
       if (lane == 0) {
         if (p.trace) s_t0 = globaltimer();
-        if (tk.x >= 0) nid = atomicAdd(p.next, 1);
+        if (tk.x >= 0) nid = qlo + atomicAdd(qnext, 1);
       }
       const bool ok = tk.x >= 0 && wait_deps<CHOL>(p, tk);
       if (lane == 0) {
         __threadfence();
         s_go = ok;
         s_id[cur ^ 1] = nid;
-        s_task[cur ^ 1] = (tk.x >= 0 && nid < p.ntasks) ? p.tasks[nid] : kNone;
+        s_task[cur ^ 1] = (tk.x >= 0 && nid < qhi) ? p.tasks[nid] : kNone;
         if (p.trace) s_t1 = globaltimer();
       }
     }
@@ -1003,22 +1029,29 @@ bool eligible(int n, int by, int bx) {
 // clipped to the trailing rows, so a region's tiles are updated by the same
 // region task at every step.
 //
-// Order: step by step (every task of step k depends only on walker step k
-// and on step k-1 tasks, so the queue never waits on a task behind it, and
-// walker step k+1 needs only step-k tasks and walker step k: no deadlock).
-// Inside a step the tasks the walker needs next come first — the L21
-// regions, U(k,k+2), the GEMM regions of tiles (k+2,k+1), (k+1,k+2),
-// (k+2,k+2) — then the rest, column by column.
-std::vector<int4> build_tasks(bool chol, int n, int by, int bx) {
+// Two queues, each in step order.  The urgent queue (served by a few
+// dedicated CTAs) holds what the walker needs next: per step k all L21
+// regions, U(k,k+2) and the GEMM regions touching tile rows <= k+2 in
+// columns <= k+2; the bulk queue the rest.  Deadlock-free: every task waits
+// only on earlier steps, walker steps <= its own, same-step tasks earlier in
+// its own queue, or (bulk only) same-step urgent tasks — and urgent tasks
+// never wait on same-step bulk tasks; the walker's step k+1 waits only on
+// step-k tasks.  So the urgent work of step k is never stuck behind the
+// bulk of step k-1.  Returns urgent ++ bulk; *n_urgent = urgent count.
+std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
   const int T = bx, nt = n / bx;
-  std::vector<int4> out;
-  out.reserve(static_cast<size_t>(count_tasks(chol, n, by, bx)));
-  std::vector<char> done;
+  std::vector<int4> urg, bulk;
+  bulk.reserve(static_cast<size_t>(count_tasks(chol, n, by, bx)));
   for (int k = 0; k + 1 < nt; ++k) {
     const int pe = (k + 1) * T;
-    std::vector<int4> step;
     auto task = [&](int kind, int r0, int r1, int j) {
-      if (r0 < r1) step.push_back(make_int4(kind | (j << 2), k, r0, r1));
+      if (r0 >= r1) return;
+      const int4 t = make_int4(kind | (j << 2), k, r0, r1);
+      bool u;
+      if (kind == kTrsmU) u = j == k + 2;
+      else if (kind == kTrsmL) u = true;  // any GEMM region may straddle into any of them
+      else u = j <= k + 2 && r0 / T <= k + 2;
+      (u ? urg : bulk).push_back(t);
     };
     std::vector<std::pair<int, int>> reg;  // row regions: multiples of by, clipped
     for (int r = (pe / by) * by; r < n; r += by) reg.emplace_back(std::max(r, pe), std::min(n, r + by));
@@ -1031,27 +1064,20 @@ std::vector<int4> build_tasks(bool chol, int n, int by, int bx) {
         if (j == k + 1) r0 = std::max(r0, pe + T);        // tile (k+1,k+1): the walker
         task(kGemm, r0, rg.second, j);
       }
-    // urgent first (stable): all L21 regions (any GEMM region may straddle
-    // into them), U(k,k+2), and the GEMM regions touching tile rows <= k+2
-    // in columns <= k+2
-    auto urgent = [&](const int4& t) {
-      const int kind = t.x & 3, j = t.x >> 2;
-      if (kind == kTrsmU) return j == k + 2;
-      if (kind == kTrsmL) return true;
-      return j <= k + 2 && t.z / T <= k + 2;
-    };
-    std::stable_partition(step.begin(), step.end(), urgent);
-    out.insert(out.end(), step.begin(), step.end());
   }
-  return out;
+  if (n_urgent) *n_urgent = static_cast<int>(urg.size());
+  urg.insert(urg.end(), bulk.begin(), bulk.end());
+  return urg;
 }
 
 cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
-  const std::vector<int4> tasks = build_tasks(chol, n, by, bx);
+  int nurg = 0;
+  const std::vector<int4> tasks = build_tasks(chol, n, by, bx, &nurg);
   const int nt = n / bx;
   w->ntasks = static_cast<int>(tasks.size());
+  w->nurgent = nurg;
   w->nsteps = n / bx;
-  w->cnt_bytes = (static_cast<size_t>(nt) * nt + 2) * sizeof(int);
+  w->cnt_bytes = (static_cast<size_t>(nt) * nt + 3) * sizeof(int);
   cudaError_t e = cudaMalloc(&w->tasks, tasks.size() * sizeof(int4));
   if (e != cudaSuccess) return e;
   e = cudaMemcpy(w->tasks, tasks.data(), tasks.size() * sizeof(int4), cudaMemcpyHostToDevice);
@@ -1068,7 +1094,10 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  w->grid = 1 + std::max(0, std::min(sms - 1, w->ntasks));  // walker + queue workers
+  // walker + urgent-queue workers + bulk-queue workers
+  w->nuw = nurg > 0 ? std::max(1, std::min(16, (sms - 1) / 8)) : 0;
+  const int nbulk = w->ntasks - nurg;
+  w->grid = 1 + w->nuw + std::max(0, std::min(sms - 1 - w->nuw, nbulk));
   return cudaSuccess;
 }
 
@@ -1094,10 +1123,12 @@ cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long l
   prm.tasks = w.tasks;
   prm.ntasks = w.ntasks;
   prm.cnt = w.cnt;
-  prm.next = w.cnt + static_cast<size_t>(nt) * nt;
+  prm.next = w.cnt + static_cast<size_t>(nt) * nt;  // [0] urgent, [2] bulk
   prm.abort = prm.next + 1;
   prm.info = info;
   prm.trace = w.trace;
+  prm.nurgent = w.nurgent;
+  prm.nuw = w.nuw;
   prm.solve = w.solve;
   const int nf = (bx + 7) / 8;
   return chol ? launch_nf<true>(nf, prm, w.grid, s) : launch_nf<false>(nf, prm, w.grid, s);

@@ -44,13 +44,16 @@ bool eligible(int n, int by, int bx);
 
 // Host-built task list in dependency-respecting priority order
 // (int4 {kind | j << 2, k, r0, r1}).
-std::vector<int4> build_tasks(bool chol, int n, int by, int bx);
+// Urgent queue first, then bulk; *n_urgent (may be null) gets the urgent count.
+std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent);
 
 struct Workspace {
   int4* tasks = nullptr;   // device task list
   int ntasks = 0;
   int nsteps = 0;          // n / bx: walker steps (trace rows after the tasks)
-  int* cnt = nullptr;      // nt*nt tile counters + 1 task counter + 1 abort flag
+  int nurgent = 0;         // urgent-queue tasks (the first nurgent of the list)
+  int nuw = 0;             // CTAs serving the urgent queue
+  int* cnt = nullptr;      // nt*nt tile counters + urgent counter, abort flag, bulk counter
   size_t cnt_bytes = 0;
   int grid = 0;
   unsigned long long* trace = nullptr;  // TT_DAG_TRACE=1: per-task timestamps

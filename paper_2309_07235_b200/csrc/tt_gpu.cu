@@ -860,7 +860,7 @@ int tt_dev_fill_uniform(tt_ctx* ctx, double* a, int rows, int cols, int ld, long
 
 int tt_dag_tasks(int kernel, int n, int by, int bx, int* out, int cap) {
   if (!tt::dag::eligible(n, by, bx)) return -1;
-  const std::vector<int4> v = tt::dag::build_tasks(kernel != TT_KERNEL_LU, n, by, bx);
+  const std::vector<int4> v = tt::dag::build_tasks(kernel != TT_KERNEL_LU, n, by, bx, nullptr);
   if (out) {
     const size_t m = std::min(v.size(), static_cast<size_t>(std::max(cap, 0)));
     for (size_t i = 0; i < m; ++i) {
@@ -871,6 +871,13 @@ int tt_dag_tasks(int kernel, int n, int by, int bx, int* out, int cap) {
     }
   }
   return static_cast<int>(v.size());
+}
+
+int tt_dag_urgent(int kernel, int n, int by, int bx) {
+  if (!tt::dag::eligible(n, by, bx)) return -1;
+  int nu = 0;
+  tt::dag::build_tasks(kernel != TT_KERNEL_LU, n, by, bx, &nu);
+  return nu;
 }
 
 int tt_dag_trace(tt_ctx* ctx, unsigned long long* out, int cap) {

@@ -80,35 +80,40 @@ def walker_signals(k, T, nt, chol):
     return sig
 
 
-def interleaved(tasks, nt, T, chol):
-    """The kernel's semantics sequentialised: the walker runs each step as soon
-    as its dependencies hold; the queue is taken strictly in list order.  A
-    queue task whose wait condition does not hold when it is reached (with
-    the walker stuck) would deadlock the persistent kernel."""
+def interleaved(tasks, nt, T, chol, nurg):
+    """A sequential execution the kernel's queues admit: per step k the walker,
+    then step k of the urgent queue, then step k of the bulk queue, each queue
+    in its own order.  Every wait condition must hold when its task is
+    reached; together with the per-queue step order this is the kernel's
+    deadlock-freedom argument (see build_tasks)."""
+    urg, bulk = tasks[:nurg], tasks[nurg:]
+    for q in (urg, bulk):
+        assert np.all(np.diff(q[:, 1]) >= 0), "queue not in step order"
     cnt = np.zeros((nt, nt), dtype=np.int64)
-    out, s = [], 0
-
-    def walker_ready(s):
-        return all(cnt[tile] >= nd for tile, nd in walker_needs(s, T, nt, chol))
-
-    def run_walker():
-        nonlocal s
-        while s < nt and walker_ready(s):
-            out.append(("W", s))
-            for tile, rows in walker_signals(s, T, nt, chol).items():
-                cnt[tile] += rows
-            s += 1
-
-    for t in tasks:
-        run_walker()
-        kind, j, k, r0, r1 = decode(t)
-        for tile, nd in needs(kind, j, k, r0, r1, T, chol):
-            assert cnt[tile] >= nd, ("deadlock", t, tile, nd, cnt[tile], "walker at", s)
-        out.append(("Q", t))
-        for tile, rows in signals(kind, j, k, r0, r1, T).items():
+    out = []
+    iu = ib = 0
+    for k in range(nt):
+        for tile, nd in walker_needs(k, T, nt, chol):
+            assert cnt[tile] >= nd, ("walker", k, tile, nd, cnt[tile])
+        out.append(("W", k))
+        for tile, rows in walker_signals(k, T, nt, chol).items():
             cnt[tile] += rows
-    run_walker()
-    assert s == nt, ("walker stuck at", s)
+        for q, idx in ((urg, "u"), (bulk, "b")):
+            i = iu if idx == "u" else ib
+            while i < len(q) and q[i][1] == k:
+                t = q[i]
+                kind, j, kk, r0, r1 = decode(t)
+                for tile, nd in needs(kind, j, kk, r0, r1, T, chol):
+                    assert cnt[tile] >= nd, (idx, t, tile, nd, cnt[tile])
+                out.append(("Q", t))
+                for tile, rows in signals(kind, j, kk, r0, r1, T).items():
+                    cnt[tile] += rows
+                i += 1
+            if idx == "u":
+                iu = i
+            else:
+                ib = i
+    assert iu == len(urg) and ib == len(bulk)
     return out
 
 
@@ -120,7 +125,8 @@ def test_task_order_and_coverage(kernel, n, by, bx):
     T, nt = bx, n // bx
     assert not np.any((tasks[:, 0] & 3) == DIAG)  # DIAG belongs to the walker
     cnt = np.zeros((nt, nt), dtype=np.int64)
-    for what, t in interleaved(tasks, nt, T, chol):
+    nurg = _lib.load().tt_dag_urgent(_lib.KERNEL_IDS[kernel], n, by, bx)
+    for what, t in interleaved(tasks, nt, T, chol, nurg):
         if what == "W":
             need, sig = walker_needs(t, T, nt, chol), walker_signals(t, T, nt, chol)
         else:
@@ -142,7 +148,7 @@ def test_task_order_and_coverage(kernel, n, by, bx):
                 assert cnt[i, jj] == (min(i, jj) + 1) * T, (i, jj)
 
 
-def run_tasks_numpy(a, tasks, bx, chol):
+def run_tasks_numpy(a, tasks, bx, chol, nurg):
     a = a.copy()
     T = bx
     nt = a.shape[0] // T
@@ -168,7 +174,7 @@ def run_tasks_numpy(a, tasks, bx, chol):
             upd = np.where(rows >= cols, upd, a[r0:r1, jT:jT + T])
         a[r0:r1, jT:jT + T] = upd
 
-    for what, t in interleaved(tasks, nt, T, chol):
+    for what, t in interleaved(tasks, nt, T, chol, nurg):
         if what == "W":  # walker step k
             k = t
             kT = k * T
@@ -200,7 +206,8 @@ def run_tasks_numpy(a, tasks, bx, chol):
 def test_task_semantics_reproduce_reference(kernel, n, by, bx):
     chol = kernel == "cholesky"
     a0 = oracle.gen_spd(n, 5)
-    out = run_tasks_numpy(a0, _lib.dag_tasks(kernel, n, by, bx), bx, chol)
+    nurg = _lib.load().tt_dag_urgent(_lib.KERNEL_IDS[kernel], n, by, bx)
+    out = run_tasks_numpy(a0, _lib.dag_tasks(kernel, n, by, bx), bx, chol, nurg)
     ref = a0.copy()
     if chol:
         oracle.cholesky_factor_inplace(ref, by, bx)
