@@ -3,7 +3,9 @@
 
 Headline workload (configs[1]): LU without pivoting, PolyBench LARGE N=2000,
 fixed block (by, bx) = BENCH_LU_BLOCK, inputs gen_spd(2000, seed=1).  A step
-is one in-place factorisation of one resident input matrix.  Inputs cycle
+is one in-place factorisation of one resident input matrix: ONE launch of the
+persistent tile-DAG kernel (paper_2309_07235_b200/csrc/dag_factor.cu; walker
+CTA on the diagonal chain + queue workers on the bulk TRSM/GEMM tasks).  Inputs cycle
 through a ring of W+K distinct device copies (each step's input is cold in
 L2: the ring is W+K x 32 MB and every copy was written during setup), so
 there is no restore copy in the timed region.
@@ -12,9 +14,12 @@ value   = algorithmic (2/3) n^3 flop per step x steps x ranks / max-over-ranks
           device time (CUDA events on the launching stream)
 e2e     = same metric through the reference-facing C-ABI drop-in
           tt_lu_factor_inplace with pinned host buffers (H2D + factor + D2H)
-roofline: bound "tensor" (fp64 DMMA); peak = the measured DMMA issue rate on
-          this pool's B200s (profiles/fp64_peak_r01.jsonl, 37.05 TFLOP/s,
-          MEASURED_PEAKS.json has no fp64 entry).
+roofline: bound "tensor" (fp64 DMMA); the dominant (only) kernel of a step
+          is the persistent factorisation kernel, so achieved = (2/3) n^3 per
+          launch / its CUDA-event launch time; peak = the measured DMMA issue
+          rate on this pool's B200s (profiles/fp64_peak_r01.jsonl, 37.05
+          TFLOP/s; MEASURED_PEAKS.json has no fp64 entry); traffic = DRAM
+          bytes of one ncu --set full capture (profiles/ncu_traffic.json).
 Multi-GPU: LU is single-GPU per factorisation (north_star), so N ranks run
 N independent replicas ("replicas only", scaling "weak").
 
@@ -332,9 +337,9 @@ def run_gpu_arm(args, rank, world, local):
         import oracle
         res = oracle.lu_residual_packed(host_a, host[0])  # O(n^3) CPU check of one e2e output
         ref_fac = host_a.copy()
-        # dominant-kernel live measurement: the step-0 trailing update (M=N=n-bx, K=bx)
-        dom = dominant_trailing_gemm(ctx, lib, torch, n, by, bx, sptr, stream)
         achieved = lu_flops(n) / (ms / args.steps * 1e-3) / 1e12
+        traffic = ncu_traffic(f"lu_nopiv_large_n{n}_fixed_block")
+        sched = schedule_info(lib, n, by, bx)
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -345,10 +350,12 @@ def run_gpu_arm(args, rank, world, local):
                        "l2_policy": f"ring of {ring_len} distinct resident inputs (32 MB each), 256 MB L2 flush after restoring them; every timed step's input is cold in L2"},
             "pct_of_fp64_peak": 100.0 * achieved / FP64_PEAK_TFLOPS,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                         "launch_unit": "one CUDA-graph launch = one full factorisation (the instantiated schedule)",
-                         "peak_source": FP64_PEAK_SOURCE,
-                         "dominant_kernel": dom},
+                         "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                         "traffic": traffic,
+                         "kernel": sched["kernel"],
+                         "launch_unit": "one launch = one full factorisation ((2/3) n^3 flop); timed with CUDA events on the launching stream",
+                         "peak_source": FP64_PEAK_SOURCE},
+            "schedule": sched,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": n * n * 8,
                     "d2h_bytes_per_step": n * n * 8, "steps": e2e_steps,
                     "api": "tt_lu_factor_inplace (C ABI drop-in for lu_factor_inplace)"},
@@ -359,32 +366,25 @@ def run_gpu_arm(args, rank, world, local):
     return line, ctx
 
 
-def dominant_trailing_gemm(ctx, lib, torch, n, by, bx, sptr, stream):
-    """Times the largest trailing-update DMMA GEMM of the schedule on its own."""
-    M = n - bx
-    a = torch.rand((n, n), dtype=torch.float64, device="cuda")
-    reps = 20
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+def ncu_traffic(workload: str):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full capture summary, or None."""
+    f = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        return json.loads(f.read_text()).get(workload)
+    except Exception:
+        return None
 
-    def launch():
-        A = ctypes.c_void_p(a[bx:, :].data_ptr())
-        B = ctypes.c_void_p(a[:, bx:].data_ptr())
-        C = ctypes.c_void_p(a[bx:, bx:].data_ptr())
-        ctx.check(lib.tt_dev_gemm(ctx.handle, A, n, B, n, 0, C, n, M, M, bx, by_fit(M, by),
-                                  by_fit(M, bx), -1, 1, sptr))
 
-    for _ in range(3):
-        launch()
-    e0.record(stream)
-    for _ in range(reps):
-        launch()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
-    flops = 2.0 * M * M * bx
-    return {"name": f"dgemm_kernel (trailing update step 0: M=N={M}, K={bx}, region ({by},{bx}))",
-            "achieved_tflops": flops / (ms * 1e-3) / 1e12, "avg_launch_ms": ms,
-            "frac": flops / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS}
+def schedule_info(lib, n, by, bx):
+    """Which schedule the knob setting runs on (persistent DAG or launch graph)."""
+    ntasks = lib.tt_dag_tasks(0, n, by, bx, None, 0)
+    if ntasks < 0:
+        return {"kind": "graph", "kernel": "panel/trsm/dgemm graph (schedules.cu)"}
+    nt = n // bx
+    return {"kind": "persistent tile-DAG", "kernel": f"dag_kernel<{(bx + 7) // 8}, LU>",
+            "queue_tasks": ntasks, "urgent_tasks": lib.tt_dag_urgent(0, n, by, bx),
+            "walker_steps": nt}
 
 
 def by_fit(extent, f):
@@ -405,8 +405,8 @@ def extra_workloads(ctx, quick: bool):
          mm3_flops(800, 900, 1000, 1100, 1200)),
         ("mm3_extralarge", KernelCase("3mm", 1600, 1800, 2000, 2200, 2400), (64, 125, 125, 120, 64, 120),
          mm3_flops(1600, 1800, 2000, 2200, 2400)),
-        ("cholesky_extralarge", KernelCase("cholesky", 4000), (160, 160), chol_flops(4000)),
-        ("lu_extralarge", KernelCase("lu", 4000), (160, 160), lu_flops(4000)),
+        ("cholesky_extralarge", KernelCase("cholesky", 4000), (500, 50), chol_flops(4000)),
+        ("lu_extralarge", KernelCase("lu", 4000), (160, 50), lu_flops(4000)),
     ]
     for name, kase, cfg, flops in cases:
         try:
