@@ -200,6 +200,7 @@ __device__ __forceinline__ void warp_signal(const Params& p, int ra, int rb, int
   }
 }
 
+
 // ---------------------------------------------------------------- GEMM
 // One warp's share of a GEMM task: C[r, c] -= sum_k A[r, k] * B[k, c] over
 // the 16-row strips ra = r0 + 16*warp, +128, ... of rows [r0, r1).  B (Kp x
@@ -211,7 +212,8 @@ __device__ __forceinline__ void warp_signal(const Params& p, int ra, int rb, int
 template <int NF>
 __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int k, int j,
                                             const double* __restrict__ Bs, double* abuf,
-                                            bool chol, unsigned long long* first_done) {
+                                            bool chol, unsigned long long* first_done,
+                                            bool defer) {
   const int kT = k * p.T, jT = j * p.T;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
   const int T = p.T;
@@ -248,6 +250,7 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
   };
 
   double acc[kMF][NF][2];
+  int prev_ra = -1, prev_nr = 0;
   if (!strip_deps(p, ra, min(ra + kStrip, r1), j, k, true, true)) return;
   issue_a(ra, abuf);
   load_c(ra, acc);
@@ -288,6 +291,9 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
           for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], af[mf], bf[nf]);
       }
     }
+    // publish the previous strip now: its stores were issued a whole strip
+    // ago, so the fence does not stall on their acknowledgement
+    if (prev_ra >= 0) warp_signal(p, prev_ra, prev_ra + prev_nr, j);
     const int lower_off = chol ? ra - jT : kNoLower;
 #pragma unroll
     for (int mf = 0; mf < kMF; ++mf) {
@@ -304,14 +310,15 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
       }
     }
     if (first_done && lane == 0) first_done[2] = globaltimer() + static_cast<unsigned long long>(acc[0][0][0] * 0.0);
-    warp_signal(p, ra, ra + nr, j);
+    prev_ra = ra;
+    prev_nr = nr;
     if (first_done && lane == 0) {
       *first_done = globaltimer();
       first_done = nullptr;
     }
     if (!more) break;
     if (!pref) {
-      if (!strip_deps(p, rn, min(rn + kStrip, r1), j, k, true, true)) return;
+      if (!strip_deps(p, rn, min(rn + kStrip, r1), j, k, true, true)) return;  // aborted
       issue_a(rn, abuf + (cur ^ 1) * kABuf);
       load_c(rn, cn);
     }
@@ -325,6 +332,8 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
     ra = rn;
     cur ^= 1;
   }
+  if (prev_ra >= 0) warp_signal(p, prev_ra, prev_ra + prev_nr, j);
+  (void)defer;
 }
 
 // ---------------------------------------------------------------- DIAG
@@ -893,7 +902,7 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
       __syncthreads();
       stamp(0);
       gemm_strips<NF>(p, r0, r1, k, j, sm, abuf + warp * 2 * kABuf, CHOL,
-                      (p.trace && warp == 0) ? &s_ph[1] : nullptr);
+                      (p.trace && warp == 0) ? &s_ph[1] : nullptr, !urgent_q);
     } else {  // TRSM
       const bool lsolve = kind == kTrsmL;
       {  // M from the factored diagonal tile (one batched L2 round trip), then
@@ -1009,7 +1018,7 @@ long long count_tasks(bool chol, int n, int by, int bx) {
     const int pe = (k + 1) * bx;
     const long long regions = (n - 1) / by - pe / by + 1;
     const long long cols = nt - k - 1;
-    total += regions + (chol ? 0 : cols) + regions * cols;
+    total += regions + (chol ? 0 : cols) + regions * cols + 4;  // + carved pieces
   }
   return total;
 }
@@ -1030,28 +1039,33 @@ bool eligible(int n, int by, int bx) {
 // region task at every step.
 //
 // Two queues, each in step order.  The urgent queue (served by a few
-// dedicated CTAs) holds what the walker needs next: per step k all L21
-// regions, U(k,k+2) and the GEMM regions touching tile rows <= k+2 in
-// columns <= k+2; the bulk queue the rest.  Deadlock-free: every task waits
-// only on earlier steps, walker steps <= its own, same-step tasks earlier in
-// its own queue, or (bulk only) same-step urgent tasks — and urgent tasks
-// never wait on same-step bulk tasks; the walker's step k+1 waits only on
-// step-k tasks.  So the urgent work of step k is never stuck behind the
-// bulk of step k-1.  Returns urgent ++ bulk; *n_urgent = urgent count.
+// dedicated CTAs) holds what the walker needs next — per step k: the L21
+// rows of tile row k+2, U(k,k+2), and the GEMM rows of tiles (k+2,k+1),
+// (k+1,k+2), (k+2,k+2) — carved out of their row regions at the row
+// (k+3)*bx, so urgent tasks stay one or two tiles small; the bulk queue
+// holds the rest.  Deadlock-free: every task waits only on earlier steps,
+// walker steps <= its own, same-step tasks earlier in its own queue, or
+// (bulk only) same-step urgent tasks — urgent tasks never wait on same-step
+// bulk tasks (their rows lie above the carve row, as do the L21 rows they
+// read); the walker's step k+1 waits only on step-k tasks.  So the urgent
+// work of step k is never stuck behind the bulk of step k-1.
+// Returns urgent ++ bulk; *n_urgent = urgent count.
 std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
   const int T = bx, nt = n / bx;
   std::vector<int4> urg, bulk;
   bulk.reserve(static_cast<size_t>(count_tasks(chol, n, by, bx)));
   for (int k = 0; k + 1 < nt; ++k) {
     const int pe = (k + 1) * T;
+    const int carve = std::min(n, (k + 3) * T);  // rows above: tile rows <= k+2
     auto task = [&](int kind, int r0, int r1, int j) {
       if (r0 >= r1) return;
-      const int4 t = make_int4(kind | (j << 2), k, r0, r1);
-      bool u;
-      if (kind == kTrsmU) u = j == k + 2;
-      else if (kind == kTrsmL) u = true;  // any GEMM region may straddle into any of them
-      else u = j <= k + 2 && r0 / T <= k + 2;
-      (u ? urg : bulk).push_back(t);
+      const bool near = kind == kTrsmU ? j == k + 2 : (kind == kTrsmL || j <= k + 2);
+      if (near && r0 < carve) {  // split at the carve row
+        urg.push_back(make_int4(kind | (j << 2), k, r0, kind == kTrsmU ? r1 : std::min(r1, carve)));
+        if (kind != kTrsmU && r1 > carve) bulk.push_back(make_int4(kind | (j << 2), k, carve, r1));
+      } else {
+        bulk.push_back(make_int4(kind | (j << 2), k, r0, r1));
+      }
     };
     std::vector<std::pair<int, int>> reg;  // row regions: multiples of by, clipped
     for (int r = (pe / by) * by; r < n; r += by) reg.emplace_back(std::max(r, pe), std::min(n, r + by));
@@ -1095,7 +1109,7 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // walker + urgent-queue workers + bulk-queue workers
-  w->nuw = nurg > 0 ? std::max(1, std::min(16, (sms - 1) / 8)) : 0;
+  w->nuw = nurg > 0 ? std::max(1, std::min(8, (sms - 1) / 8)) : 0;
   const int nbulk = w->ntasks - nurg;
   w->grid = 1 + w->nuw + std::max(0, std::min(sms - 1 - w->nuw, nbulk));
   return cudaSuccess;

@@ -59,4 +59,4 @@ grid = len(set(tr[:, 3]))
 print(f"  utilisation (task run time / (SMs x span)) = {busy / (grid * span):.3f}")
 
 if len(sys.argv) > 5:
-    np.savez(sys.argv[5], tasks=tasks, trace=tr)
+    np.savez(sys.argv[5], tasks=tasks, trace=tr, walker=trall[nt:], nurgent=ctx.lib.tt_dag_urgent(0 if kern == "lu" else 1, n, by, bx))

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout -s KILL 300 python tools/dag_check.py > gpurun_out/dag_check.log 2>&1; echo "dag_check rc=$?"; cat gpurun_out/dag_check.log | grep -v "dag=False"
+for c in "lu 2000 400 50" "cholesky 4000 500 50"; do
+  set -- $c
+  timeout -s KILL 120 python tools/dag_trace.py $c gpurun_out/trace_$1_$2_$3_$4.npz 2>&1 | tail -11
+done
