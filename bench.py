@@ -405,7 +405,7 @@ def extra_workloads(ctx, quick: bool):
          mm3_flops(800, 900, 1000, 1100, 1200)),
         ("mm3_extralarge", KernelCase("3mm", 1600, 1800, 2000, 2200, 2400), (64, 125, 125, 120, 64, 120),
          mm3_flops(1600, 1800, 2000, 2200, 2400)),
-        ("cholesky_extralarge", KernelCase("cholesky", 4000), (500, 50), chol_flops(4000)),
+        ("cholesky_extralarge", KernelCase("cholesky", 4000), (250, 50), chol_flops(4000)),
         ("lu_extralarge", KernelCase("lu", 4000), (160, 50), lu_flops(4000)),
     ]
     for name, kase, cfg, flops in cases:

@@ -567,10 +567,13 @@ __device__ __forceinline__ void tile_store(const double* D, double* __restrict__
 // transposed U12 solve).  M (Tp x Tp upper triangular, identity-padded) and
 // the inverses of its 8x8 diagonal blocks are in shared memory.  Blocked by
 // 8 columns: R_b = S_b - X_<b * M_<b,b (DMMA), X_b = R_b * inv(M_bb) (DMMA).
-template <int NF, bool SMEM = false>
+// MMODE: 0 = M[r][c] = Ms[r*kNP + c]; 1 = M[r][c] = Ms[c*kNP + r] (M is the
+// transpose of the stored tile); 2 = as 1, scaled by msc[r] (Cholesky L^T).
+template <int NF, bool SMEM = false, int MMODE = 0>
 __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long rs, long long cs,
                                           int nrows, int T, const double* __restrict__ Ms,
-                                          const double* __restrict__ Minv) {
+                                          const double* __restrict__ Minv,
+                                          const double* __restrict__ msc = nullptr) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double ra[NF][kMF][2];
 #pragma unroll
@@ -604,7 +607,9 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
     for (int bb = 0; bb < b; ++bb)
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        const double m = Ms[(bb * 8 + 4 * s + t) * kNP + b * 8 + g];
+        const int mr = bb * 8 + 4 * s + t, mc = b * 8 + g;
+        double m = MMODE == 0 ? Ms[mr * kNP + mc] : Ms[mc * kNP + mr];
+        if (MMODE == 2) m *= msc[mr];
 #pragma unroll
         for (int mf = 0; mf < kMF; ++mf) dmma_8x8x4(acc[mf][0], acc[mf][1], xa[bb][mf][s], m);
       }
@@ -664,8 +669,6 @@ __device__ void walker(const Params& p, double* dsm) {
   double* D = dsm;                          // tile (k,k)
   double* Lt = dsm + kSmemB;                // tile (k+1,k): A21 -> L21
   double* Ut = Lt + kSmemB;                 // tile (k,k+1): A12 -> U12 (LU)
-  double* Mu = Ut + kSmemB;                 // M of the L21 solve
-  double* Ml = Mu + kSmemB;                 // M of the U12 solve (LU)
   double* rk = dsm + kSmemB + kSmemA + 9 * 64 + 2 * kPB;  // 128
   double* inv = rk + 128;                   // 1024: DIAG block inverses
   double* invX = inv + 1024;                // 512: inverses for the second solve
@@ -750,17 +753,9 @@ __device__ void walker(const Params& p, double* dsm) {
         vl[u] = in ? __ldcg(al + static_cast<long long>(x) * ld + y) : 0.0;
         vu[u] = (!CHOL && in) ? __ldcg(au + static_cast<long long>(x) * ld + y) : 0.0;
       }
-      // M of the solves from the factored tile (diagonal never read)
-      for (int e = tid; e < Tp * Tp; e += kThreads) {
-        const int kk = e / Tp, c = e - kk * Tp;
-        const bool up = c > kk && c < T;
-        if (CHOL) {
-          Mu[kk * kNP + c] = up ? D[c * kNP + kk] * rk[64 + kk] : 0.0;  // L^T (scaled)
-        } else {
-          Mu[kk * kNP + c] = up ? D[kk * kNP + c] : 0.0;  // U11
-          Ml[kk * kNP + c] = up ? D[c * kNP + kk] : 0.0;  // L11^T (unit)
-        }
-      }
+      // the solves read M straight from the factored tile D: U11 = upper(D),
+      // L11^T = lower(D)^T (Cholesky scaled by l_kk); only strictly-upper
+      // entries of M between 8-blocks are read, and D is identity-padded
       // block inverses of the second M: LU inv(L_bb^T) = inv(L_bb)^T;
       // Cholesky inv(diag(l) L_bb^T) = inv(L_bb)^T diag(1/l)
       for (int e = tid; e < NF * 64; e += kThreads) {
@@ -785,10 +780,14 @@ __device__ void walker(const Params& p, double* dsm) {
       const int c0 = sw * kStrip;
       if (c0 < T) {
         const int nr = min(kStrip, T - c0);
-        if (warp < 4)
-          warp_trsm<NF, true>(Lt + c0 * kNP, kNP, 1, nr, T, Mu, CHOL ? invX : inv);
-        else if (!CHOL)
-          warp_trsm<NF, true>(Ut + c0, 1, kNP, nr, T, Ml, invX);
+        if (warp < 4) {
+          if (CHOL)
+            warp_trsm<NF, true, 2>(Lt + c0 * kNP, kNP, 1, nr, T, D, invX, rk + 64);
+          else
+            warp_trsm<NF, true, 0>(Lt + c0 * kNP, kNP, 1, nr, T, D, inv);
+        } else if (!CHOL) {
+          warp_trsm<NF, true, 1>(Ut + c0, 1, kNP, nr, T, D, invX);
+        }
       }
     }
     __syncthreads();
@@ -1038,6 +1037,17 @@ bool eligible(int n, int by, int bx) {
 // clipped to the trailing rows, so a region's tiles are updated by the same
 // region task at every step.
 //
+// Width (in tiles beyond the walker's) of the band carved into the urgent
+// queue; TT_DAG_BAND overrides (tuning aid).
+int urgent_band() {
+  static const int b = [] {
+    const char* v = std::getenv("TT_DAG_BAND");
+    const int x = v ? std::atoi(v) : 0;
+    return x >= 1 && x <= 16 ? x : 3;
+  }();
+  return b;
+}
+
 // Two queues, each in step order.  The urgent queue (served by a few
 // dedicated CTAs) holds what the walker needs next — per step k: the L21
 // rows of tile row k+2, U(k,k+2), and the GEMM rows of tiles (k+2,k+1),
@@ -1052,14 +1062,15 @@ bool eligible(int n, int by, int bx) {
 // Returns urgent ++ bulk; *n_urgent = urgent count.
 std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
   const int T = bx, nt = n / bx;
+  const int band = urgent_band();
   std::vector<int4> urg, bulk;
   bulk.reserve(static_cast<size_t>(count_tasks(chol, n, by, bx)));
   for (int k = 0; k + 1 < nt; ++k) {
     const int pe = (k + 1) * T;
-    const int carve = std::min(n, (k + 3) * T);  // rows above: tile rows <= k+2
+    const int carve = std::min(n, (k + 1 + band) * T);  // rows above: tile rows <= k+band
     auto task = [&](int kind, int r0, int r1, int j) {
       if (r0 >= r1) return;
-      const bool near = kind == kTrsmU ? j == k + 2 : (kind == kTrsmL || j <= k + 2);
+      const bool near = kind == kTrsmU ? j <= k + band : (kind == kTrsmL || j <= k + band);
       if (near && r0 < carve) {  // split at the carve row
         urg.push_back(make_int4(kind | (j << 2), k, r0, kind == kTrsmU ? r1 : std::min(r1, carve)));
         if (kind != kTrsmU && r1 > carve) bulk.push_back(make_int4(kind | (j << 2), k, carve, r1));
@@ -1109,7 +1120,11 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // walker + urgent-queue workers + bulk-queue workers
-  w->nuw = nurg > 0 ? std::max(1, std::min(8, (sms - 1) / 8)) : 0;
+  {
+    const char* v = std::getenv("TT_DAG_URGENT_CTAS");
+    const int want = v ? std::atoi(v) : 8;
+    w->nuw = nurg > 0 ? std::max(1, std::min(want, sms / 2)) : 0;
+  }
   const int nbulk = w->ntasks - nurg;
   w->grid = 1 + w->nuw + std::max(0, std::min(sms - 1 - w->nuw, nbulk));
   return cudaSuccess;
