@@ -209,26 +209,41 @@ __device__ __forceinline__ void warp_signal(const Params& p, int ra, int rb, int
 // (registers) are in flight while this strip's DMMAs run; the strip is
 // published (fence + red.release) right after its stores.  Stores only
 // where row + lower_off >= col (Cholesky diagonal tiles).
+// Operands of a strip task: rows r of [r0, r1) (global rows: tile counters)
+// read A from A0 + (r - r0)*lda (T columns) and update C at C0 + (r - r0)*ldc
+// (T columns of tile column cj); beta = 0 starts from zero instead of C.
+// Dependencies per strip: stage k-1 of the C tiles, plus (gemm) the L tiles
+// (i, k) final.  The product accumulated is C - A*B.
+struct StripOps {
+  const double* A0;
+  long long lda;
+  double* C0;
+  long long ldc;
+  int cj;      // tile column of C (counters)
+  bool gemm;   // also wait for L(i,k) final
+  bool beta;   // load C
+};
+
 template <int NF>
-__device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int k, int j,
+__device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int k,
+                                            const StripOps& op,
                                             const double* __restrict__ Bs, double* abuf,
-                                            bool chol, unsigned long long* first_done,
-                                            bool defer) {
-  const int kT = k * p.T, jT = j * p.T;
+                                            bool chol, unsigned long long* first_done) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
-  const int T = p.T;
-  const long long ld = p.ld;
-  const int col0 = kT & ~1, sh = kT - col0;            // 16-byte aligned copy origin
-  const int nvec = (kT + T - col0 + 1) >> 1;           // 16-byte vectors per row
+  const int T = p.T, j = op.cj;
+  const int jT = j * T;
+  // 16-byte aligned copy origin (lda even: every row has the same parity)
+  const int sh = static_cast<int>((reinterpret_cast<uintptr_t>(op.A0) >> 3) & 1);
+  const int nvec = (T + sh + 1) >> 1;  // 16-byte vectors per row
   int ra = r0 + warp * kStrip;
   if (ra >= r1) return;
 
   auto issue_a = [&](int rs, double* buf) {
     const int nr = min(kStrip, r1 - rs);
-    const double* src = p.a + static_cast<long long>(rs) * ld + col0;
+    const double* src = op.A0 - sh + static_cast<long long>(rs - r0) * op.lda;
     for (int e = lane; e < nr * nvec; e += 32) {
       const int r = e / nvec, v = e - r * nvec;
-      cp_async16(buf + r * kAW + 2 * v, src + static_cast<long long>(r) * ld + 2 * v);
+      cp_async16(buf + r * kAW + 2 * v, src + static_cast<long long>(r) * op.lda + 2 * v);
     }
     cp_async_commit();
   };
@@ -238,20 +253,20 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
     for (int mf = 0; mf < kMF; ++mf) {
       const int r = mf * 8 + g;
       const bool rv = r < nr;
-      const double* crow = p.a + static_cast<long long>(rs + (rv ? r : 0)) * ld + jT;
+      const double* crow = op.C0 + static_cast<long long>(rs - r0 + (rv ? r : 0)) * op.ldc;
 #pragma unroll
       for (int nf = 0; nf < NF; ++nf)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = nf * 8 + 2 * t + h;
-          cv[mf][nf][h] = (rv && c < T) ? __ldcg(crow + c) : 0.0;
+          cv[mf][nf][h] = (op.beta && rv && c < T) ? __ldcg(crow + c) : 0.0;
         }
     }
   };
 
   double acc[kMF][NF][2];
   int prev_ra = -1, prev_nr = 0;
-  if (!strip_deps(p, ra, min(ra + kStrip, r1), j, k, true, true)) return;
+  if (!strip_deps(p, ra, min(ra + kStrip, r1), j, k, op.gemm, true)) return;
   issue_a(ra, abuf);
   load_c(ra, acc);
   int cur = 0;
@@ -260,7 +275,7 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
     const bool more = rn < r1;
     double cn[kMF][NF][2];
     // prefetch the next strip now if its rows are already final, else after this one
-    const bool pref = more && strip_deps(p, rn, min(rn + kStrip, r1), j, k, true, false);
+    const bool pref = more && strip_deps(p, rn, min(rn + kStrip, r1), j, k, op.gemm, false);
     if (pref) {
       issue_a(rn, abuf + (cur ^ 1) * kABuf);
       load_c(rn, cn);
@@ -299,7 +314,7 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
     for (int mf = 0; mf < kMF; ++mf) {
       const int r = mf * 8 + g;
       if (r < nr) {
-        double* crow = p.a + static_cast<long long>(ra + r) * ld + jT;
+        double* crow = op.C0 + static_cast<long long>(ra - r0 + r) * op.ldc;
 #pragma unroll
         for (int nf = 0; nf < NF; ++nf)
 #pragma unroll
@@ -318,7 +333,7 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
     }
     if (!more) break;
     if (!pref) {
-      if (!strip_deps(p, rn, min(rn + kStrip, r1), j, k, true, true)) return;  // aborted
+      if (!strip_deps(p, rn, min(rn + kStrip, r1), j, k, op.gemm, true)) return;  // aborted
       issue_a(rn, abuf + (cur ^ 1) * kABuf);
       load_c(rn, cn);
     }
@@ -333,7 +348,6 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
     cur ^= 1;
   }
   if (prev_ra >= 0) warp_signal(p, prev_ra, prev_ra + prev_nr, j);
-  (void)defer;
 }
 
 // ---------------------------------------------------------------- DIAG
@@ -398,7 +412,10 @@ __device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* i
   double* invL = inv + 512 + b * 64;
   __syncwarp();  // converged warp: keeps the shuffles on the fast path
   double v0 = D[(p + g) * kNP + p + 2 * t], v1 = D[(p + g) * kNP + p + 2 * t + 1];
-  double rr[8], pv[8];
+  // W = I, transformed by the same row operations: ends as inv(L_bb)
+  double w0 = g == 2 * t ? 1.0 : 0.0, w1 = g == 2 * t + 1 ? 1.0 : 0.0;
+  double rr[8];
+  int fail = INT_MAX;  // first failing pivot (warp-uniform: pivots come by shuffle)
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     const double sel = (kk & 1) ? v1 : v0;
@@ -406,54 +423,42 @@ __device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* i
     const double agk = __shfl_sync(0xffffffffu, sel, g * 4 + (kk >> 1));
     const double u0 = __shfl_sync(0xffffffffu, v0, kk * 4 + t);
     const double u1 = __shfl_sync(0xffffffffu, v1, kk * 4 + t);
+    const double x0 = __shfl_sync(0xffffffffu, w0, kk * 4 + t);
+    const double x1 = __shfl_sync(0xffffffffu, w1, kk * 4 + t);
     const double r = rcp_nr(piv);
     const double m = g > kk ? agk * r : 0.0;
     if (2 * t > kk) v0 = fma(-m, u0, v0);
     if (2 * t + 1 > kk) v1 = fma(-m, u1, v1);
     if (g > kk && 2 * t == kk) v0 = m;
     if (g > kk && 2 * t + 1 == kk) v1 = m;
+    w0 = fma(-m, x0, w0);
+    w1 = fma(-m, x1, w1);
     rr[kk] = r;
-    pv[kk] = piv;
+    // the reference's failure predicates (kernels.cpp:187-190 / :297-302; NaN passes)
+    if (p + kk < T && (CHOL ? piv <= 0.0 : fabs(piv) < 1e-300)) fail = min(fail, kk);
   }
   D[(p + g) * kNP + p + 2 * t] = v0;
   D[(p + g) * kNP + p + 2 * t + 1] = v1;
-  // reciprocals and the reference's failure predicates, off the pivot chain
+  invL[g * 8 + 2 * t] = w0;
+  invL[g * 8 + 2 * t + 1] = w1;
 #pragma unroll
-  for (int kk = 0; kk < 8; ++kk) {
-    if (lane == kk && p + kk < T) {
-      rk[p + kk] = rr[kk];
-      const double piv = pv[kk];
-      if (CHOL ? piv <= 0.0 : fabs(piv) < 1e-300)
-        atomicMin(info, gcol + p + kk);  // kernels.cpp:187-190 / :297-302 (NaN passes)
-    }
-  }
+  for (int kk = 0; kk < 8; ++kk)
+    if (p + kk < T) rk[p + kk] = rr[kk];  // same value from every lane
+  if (fail != INT_MAX && lane == 0) atomicMin(info, gcol + p + fail);
   __syncwarp();
-  // inv(U_bb): lanes 0..7 (column c, back substitution); inv(L_bb) (unit
-  // lower): lanes 8..15 (column c, forward substitution)
-  if (lane < 16) {
-    const int c = lane & 7;
+  // inv(U_bb): lanes 0..7 (column c, back substitution, no divisions)
+  if (lane < 8) {
+    const int c = lane;
     double x[8];
-    if (lane < 8) {
 #pragma unroll
-      for (int ii = 7; ii >= 0; --ii) {
-        double acc = ii == c ? 1.0 : 0.0;
+    for (int ii = 7; ii >= 0; --ii) {
+      double acc = ii == c ? 1.0 : 0.0;
 #pragma unroll
-        for (int mm = ii + 1; mm < 8; ++mm) acc = fma(-D[(p + ii) * kNP + p + mm], x[mm], acc);
-        x[ii] = acc * (p + ii < T ? rk[p + ii] : 1.0);
-      }
-#pragma unroll
-      for (int ii = 0; ii < 8; ++ii) invU[ii * 8 + c] = x[ii];
-    } else {
-#pragma unroll
-      for (int ii = 0; ii < 8; ++ii) {
-        double acc = ii == c ? 1.0 : 0.0;
-#pragma unroll
-        for (int mm = 0; mm < ii; ++mm) acc = fma(-D[(p + ii) * kNP + p + mm], x[mm], acc);
-        x[ii] = acc;
-      }
-#pragma unroll
-      for (int ii = 0; ii < 8; ++ii) invL[ii * 8 + c] = x[ii];
+      for (int mm = ii + 1; mm < 8; ++mm) acc = fma(-D[(p + ii) * kNP + p + mm], x[mm], acc);
+      x[ii] = acc * (p + ii < T ? rr[ii] : 1.0);
     }
+#pragma unroll
+    for (int ii = 0; ii < 8; ++ii) invU[ii * 8 + c] = x[ii];
   }
 }
 
@@ -491,15 +496,18 @@ __device__ __forceinline__ void trail_row(double* D, int b, int nr, int ir, int 
 // overlaps the bulk of step b.  Two __syncthreads per 8 pivots.
 template <bool CHOL>
 __device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* info, double* inv,
-                                             double* rk) {
+                                             double* rk, unsigned long long* prof = nullptr) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int NB = (T + 7) >> 3;
+  long long c_panel = 0, c_step = 0, c0 = prof ? clock64() : 0;
   if (warp == 0) factor_block8<CHOL>(D, T, gcol, info, inv, rk, 0);
   __syncthreads();
+  if (prof && tid == 0) c_step += clock64() - c0;
   for (int b = 0; b + 1 < NB; ++b) {
     const int p = 8 * b, nr = NB - b - 1;
     const double* invU = inv + b * 64;
     const double* invL = inv + 512 + b * 64;
+    const long long c1 = prof ? clock64() : 0;
     // ---- panels: job < nr: L block (b+1+job, b) = A * inv(U_bb);
     //               job >= nr: U block (b, b+1+job-nr) = inv(L_bb) * A
     for (int job = warp; job < 2 * nr; job += kWarps) {
@@ -525,6 +533,7 @@ __device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* in
       }
     }
     __syncthreads();
+    const long long c2 = prof ? clock64() : 0;
     if (warp == 0) {  // look-ahead: diagonal block (b+1,b+1) first, then factor it
       trail_row(D, b, 1, 0, 0);
       __syncwarp();
@@ -532,7 +541,13 @@ __device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* in
     } else {  // the rest of step b's trailing update
       for (int ir = warp - 1; ir < nr; ir += kWarps - 1) trail_row(D, b, nr, ir, ir == 0 ? 1 : 0);
     }
+    if (prof && tid == 0) c_panel += c2 - c1;
     __syncthreads();
+    if (prof && tid == 0) c_step += clock64() - c2;
+  }
+  if (prof && tid == 0) {
+    prof[0] = c_panel;  // panels (+ barrier), cycles
+    prof[1] = c_step;   // look-ahead factor of the next block || trailing update (+ barrier)
   }
   // Cholesky: l_jj = sqrt(u_jj) (rk[64 + j]) and 1/l_jj (rk[j]) for the solves
   if (CHOL && tid < T) {
@@ -724,7 +739,8 @@ __device__ void walker(const Params& p, double* dsm) {
       __syncthreads();
     }
     stamp(k, 2);
-    diag_blocked<CHOL>(D, T, kT, p.info, inv, rk);
+    diag_blocked<CHOL>(D, T, kT, p.info, inv, rk,
+                       p.trace ? p.trace + 8 * (static_cast<long long>(p.ntasks) + k) + 6 : nullptr);
     stamp(k, 3);
     tile_store<CHOL>(D, dk, ld, T, rk, p.solve + static_cast<long long>(k) * kSolveSlot);
     __threadfence();
@@ -900,8 +916,16 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
       }
       __syncthreads();
       stamp(0);
-      gemm_strips<NF>(p, r0, r1, k, j, sm, abuf + warp * 2 * kABuf, CHOL,
-                      (p.trace && warp == 0) ? &s_ph[1] : nullptr, !urgent_q);
+      StripOps op;
+      op.A0 = p.a + static_cast<long long>(r0) * ld + kT;
+      op.lda = ld;
+      op.C0 = p.a + static_cast<long long>(r0) * ld + j * T;
+      op.ldc = ld;
+      op.cj = j;
+      op.gemm = true;
+      op.beta = true;
+      gemm_strips<NF>(p, r0, r1, k, op, sm, abuf + warp * 2 * kABuf, CHOL,
+                      (p.trace && warp == 0) ? &s_ph[1] : nullptr);
     } else {  // TRSM
       const bool lsolve = kind == kTrsmL;
       {  // M from the factored diagonal tile (one batched L2 round trip), then
@@ -1083,8 +1107,10 @@ std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
     for (const auto& rg : reg) task(kTrsmL, std::max(rg.first, pe + T), rg.second, 0);  // row k+1: walker
     if (!chol)
       for (int j = k + 2; j < nt; ++j) task(kTrsmU, 0, 1, j);
-    for (int j = k + 1; j < nt; ++j)
-      for (const auto& rg : reg) {
+    // row regions outer: a region's GEMMs need only that region's L21 rows
+    // (plus the U12 tiles), so the first GEMMs taken are the first ready
+    for (const auto& rg : reg)
+      for (int j = k + 1; j < nt; ++j) {
         int r0 = std::max(rg.first, chol ? j * T : pe);  // Cholesky: lower triangle only
         if (j == k + 1) r0 = std::max(r0, pe + T);        // tile (k+1,k+1): the walker
         task(kGemm, r0, rg.second, j);
@@ -1111,6 +1137,7 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   if (e != cudaSuccess) return e;
   e = cudaMalloc(&w->solve, static_cast<size_t>(nt) * kSolveSlot * sizeof(double));
   if (e != cudaSuccess) return e;
+
   const char* tr = std::getenv("TT_DAG_TRACE");
   if (tr && tr[0] == '1') {
     e = cudaMalloc(&w->trace, (tasks.size() + nt) * 8 * sizeof(unsigned long long));

@@ -57,7 +57,7 @@ struct Workspace {
   size_t cnt_bytes = 0;
   int grid = 0;
   unsigned long long* trace = nullptr;  // TT_DAG_TRACE=1: per-task timestamps
-  double* solve = nullptr;              // per-step TRSM operands written by DIAG
+  double* solve = nullptr;              // per-step diagonal reciprocals written by DIAG
 };
 
 // Allocates and uploads the workspace for one (kernel, n, by, bx, buffer).

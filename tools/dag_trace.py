@@ -45,6 +45,8 @@ print("  walker per step (us): wait tile %.2f, update %.2f, DIAG %.2f, store+wai
     (w[:, 1] - w[:, 0]).mean(), (w[:, 2] - w[:, 1]).mean(), (w[:, 3] - w[:, 2]).mean(),
     (w[:, 4] - w[:, 3]).mean(), (w[:, 5] - w[:, 4]).mean(), np.diff(wk[:, 0]).mean()))
 print("  walker step k=5: " + " ".join("%.1f" % x for x in wk[5]))
+wc = trall[nt + 1:-1, 6:8].astype(np.float64) / 1.96e3  # cycles -> us at 1.96 GHz
+print("  walker DIAG split (us): panels+bar %.2f, factor-next || trailing (+bar) %.2f" % (wc[:, 0].mean(), wc[:, 1].mean()))
 for kk, nm, a_, b_ in [(2, "TRSM_U", "M load+sync", "8x8 inverses+sync"), (1, "TRSM_L", "M load+sync", "8x8 inverses+sync"), (3, "GEMM", "B load+sync", "first strip (warp 0) done")]:
     mm = kind == kk
     if mm.any():
