@@ -401,9 +401,10 @@ def extra_workloads(ctx, quick: bool):
     out = {}
     proto = MeasureProtocol(2, 5, "median")
     cases = [
-        ("mm3_large_fixed", KernelCase("3mm", 800, 900, 1000, 1100, 1200), (16, 125, 125, 120, 32, 120),
+        # fixed tile configs: best of the coordinate grid search (profiles/sweep3mm_grid_r01.txt)
+        ("mm3_large_fixed", KernelCase("3mm", 800, 900, 1000, 1100, 1200), (100, 125, 125, 120, 32, 60),
          mm3_flops(800, 900, 1000, 1100, 1200)),
-        ("mm3_extralarge", KernelCase("3mm", 1600, 1800, 2000, 2200, 2400), (64, 125, 125, 120, 64, 120),
+        ("mm3_extralarge", KernelCase("3mm", 1600, 1800, 2000, 2200, 2400), (64, 125, 125, 300, 64, 240),
          mm3_flops(1600, 1800, 2000, 2200, 2400)),
         ("cholesky_extralarge", KernelCase("cholesky", 4000), (250, 50), chol_flops(4000)),
         ("lu_extralarge", KernelCase("lu", 4000), (160, 50), lu_flops(4000)),
