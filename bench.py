@@ -12,8 +12,9 @@ there is no restore copy in the timed region.
 
 value   = algorithmic (2/3) n^3 flop per step x steps x ranks / max-over-ranks
           device time (CUDA events on the launching stream)
-e2e     = same metric through the reference-facing C-ABI drop-in
-          tt_lu_factor_inplace with pinned host buffers (H2D + factor + D2H)
+e2e     = same metric through the C ABI with pinned host buffers (H2D + factor
+          + D2H every step): tt_lu_factor_batch, the pipelined batch of the
+          drop-in; the per-call drop-in tt_lu_factor_inplace is e2e.single_call
 roofline: bound "tensor" (fp64 DMMA); the dominant (only) kernel of a step
           is the persistent factorisation kernel, so achieved = (2/3) n^3 per
           launch / its CUDA-event launch time; peak = the measured DMMA issue
@@ -315,8 +316,11 @@ def run_gpu_arm(args, rank, world, local):
     check.copy_(ring[ring_len - 1])
     torch.cuda.synchronize()
 
-    # e2e through the drop-in C ABI with pinned host buffers
-    e2e_steps = max(1, min(args.steps, 10))
+    # e2e through the C ABI with pinned host buffers: the pipelined batch entry
+    # (tt_lu_factor_batch: H2D / factorisation / D2H of neighbouring matrices
+    # overlap) is the headline; the per-call drop-in (tt_lu_factor_inplace,
+    # one synchronous round trip per matrix) is reported beside it.
+    e2e_steps = max(4, min(args.steps, 20))
     host = [torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
             for _ in range(e2e_steps + 1)]
     for h in host:
@@ -324,18 +328,34 @@ def run_gpu_arm(args, rank, world, local):
     idx = ctypes.c_int(-1)
     ctx.check(lib.tt_lu_factor_inplace(ctx.handle, _lib.ptr(host[-1]), n, n, by, bx,
                                        ctypes.byref(idx)))  # warm the one-shot graph
+    ptrs = (ctypes.c_void_p * e2e_steps)(*[h.ctypes.data for h in host[:e2e_steps]])
+    fails = (ctypes.c_int * e2e_steps)()
+    for h in host[:2]:
+        h[...] = host_a
+    ctx.check(lib.tt_lu_factor_batch(ctx.handle, ptrs, 2, n, by, bx, fails))  # warm the batch graphs
+    for h in host[:2]:
+        h[...] = host_a
     barrier(world)
     t0 = time.perf_counter()
-    for i in range(e2e_steps):
-        ctx.check(lib.tt_lu_factor_inplace(ctx.handle, _lib.ptr(host[i]), n, n, by, bx,
-                                           ctypes.byref(idx)))
+    ctx.check(lib.tt_lu_factor_batch(ctx.handle, ptrs, e2e_steps, n, by, bx, fails))
     e2e_s = max_over_ranks(time.perf_counter() - t0, world)
     e2e_value = world * e2e_steps * lu_flops(n) / e2e_s / 1e9
+    single = [torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy() for _ in range(4)]
+    for h in single:
+        h[...] = host_a
+    barrier(world)
+    t0 = time.perf_counter()
+    for h in single:
+        ctx.check(lib.tt_lu_factor_inplace(ctx.handle, _lib.ptr(h), n, n, by, bx,
+                                           ctypes.byref(idx)))
+    single_s = max_over_ranks(time.perf_counter() - t0, world)
+    single_value = world * len(single) * lu_flops(n) / single_s / 1e9
 
     line = None
     if rank == 0:
         import oracle
-        res = oracle.lu_residual_packed(host_a, host[0])  # O(n^3) CPU check of one e2e output
+        res = oracle.lu_residual_packed(host_a, host[e2e_steps - 1])  # CPU check of one e2e output
+        same = bool(np.array_equal(host[0], single[0]))  # batch and per-call outputs agree bitwise
         ref_fac = host_a.copy()
         achieved = lu_flops(n) / (ms / args.steps * 1e-3) / 1e12
         traffic = ncu_traffic(f"lu_nopiv_large_n{n}_fixed_block")
@@ -358,10 +378,13 @@ def run_gpu_arm(args, rank, world, local):
             "schedule": sched,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": n * n * 8,
                     "d2h_bytes_per_step": n * n * 8, "steps": e2e_steps,
-                    "api": "tt_lu_factor_inplace (C ABI drop-in for lu_factor_inplace)"},
+                    "api": "tt_lu_factor_batch (C ABI, pipelined batch of lu_factor_inplace)",
+                    "single_call": {"value": single_value, "unit": "GFLOP/s", "steps": len(single),
+                                    "api": "tt_lu_factor_inplace (C ABI drop-in for lu_factor_inplace)"}},
             "gpu_launches": int(launches_timed),
             "clocks": clk.summary(),
-            "parity": {"lu_residual_e2e_output": res, "tolerance": 1e-12, "ok": bool(res <= 1e-12)},
+            "parity": {"lu_residual_e2e_output": res, "tolerance": 1e-12,
+                       "batch_equals_single_call": same, "ok": bool(res <= 1e-12 and same)},
         }
     return line, ctx
 

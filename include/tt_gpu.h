@@ -75,6 +75,16 @@ int tt_lu_factor_inplace(tt_ctx* ctx, double* a, int rows, int cols, int by,
 /* kernels.hpp:66  void cholesky_factor_inplace(Matrix& a, int by, int bx) */
 int tt_cholesky_factor_inplace(tt_ctx* ctx, double* a, int rows, int cols,
                                int by, int bx, int* fail_index);
+/* Pipelined batches of the two drop-ins: `count` row-major n x n host
+ * matrices (page-locked for full overlap), each factored in place; upload,
+ * factorisation and download of neighbouring matrices overlap (double-
+ * buffered on the device).  fail_index (count entries, may be NULL) gets
+ * each matrix's failing column or -1; the status is that of the first
+ * failing matrix. */
+int tt_lu_factor_batch(tt_ctx* ctx, double* const* mats, int count, int n,
+                       int by, int bx, int* fail_index);
+int tt_cholesky_factor_batch(tt_ctx* ctx, double* const* mats, int count,
+                             int n, int by, int bx, int* fail_index);
 /* kernels.hpp:43  Matrix mm3_tiled(a, b, c, d, const Configuration&)
  * dims (n,l,m,o,p) positional: A n x l, B l x m, C m x o, D o x p, G n x p. */
 int tt_mm3_tiled(tt_ctx* ctx, const double* a, const double* b,

@@ -14,9 +14,11 @@ from .kernels import (  # noqa: F401
     NumericalError,
     aggregate_samples,
     apply_env_overrides,
+    cholesky_factor_batch,
     cholesky_factor_inplace,
     cholesky_tiled,
     default_context,
+    lu_factor_batch,
     lu_factor_inplace,
     lu_tiled,
     measure,
@@ -27,6 +29,6 @@ from .kernels import (  # noqa: F401
 __all__ = [
     "Context", "DeviceError", "GpuKernelRunner", "KernelCase", "MeasureProtocol",
     "MeasurementError", "NumericalError", "aggregate_samples", "apply_env_overrides",
-    "cholesky_factor_inplace", "cholesky_tiled", "default_context", "lu_factor_inplace",
+    "cholesky_factor_batch", "cholesky_factor_inplace", "lu_factor_batch", "cholesky_tiled", "default_context", "lu_factor_inplace",
     "lu_tiled", "measure", "mm3_tiled", "unpack_lu",
 ]

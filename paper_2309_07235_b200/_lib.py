@@ -26,7 +26,7 @@ EXPORTS = (
     "tt_setup_host", "tt_setup_seeded", "tt_run", "tt_measure", "tt_measure_samples",
     "tt_get_input", "tt_residual", "tt_dev_lu", "tt_dev_cholesky", "tt_dev_mm3",
     "tt_dev_gemm", "tt_dev_fill_uniform", "tt_launch_count", "tt_build_info", "tt_dag_tasks",
-    "tt_dag_trace", "tt_dag_urgent",
+    "tt_dag_trace", "tt_dag_urgent", "tt_lu_factor_batch", "tt_cholesky_factor_batch",
 )
 
 _lib = None
@@ -73,6 +73,8 @@ def load() -> ctypes.CDLL:
         "tt_dag_tasks": (c_int, [c_int, c_int, c_int, c_int, c_int_p, c_int]),
         "tt_dag_trace": (c_int, [vp, vp, c_int]),
         "tt_dag_urgent": (c_int, [c_int, c_int, c_int, c_int]),
+        "tt_lu_factor_batch": (c_int, [vp, vp, c_int, c_int, c_int, c_int, c_int_p]),
+        "tt_cholesky_factor_batch": (c_int, [vp, vp, c_int, c_int, c_int, c_int, c_int_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -63,6 +63,8 @@ struct tt_ctx {
   DevMat e, f, g;      // mm3 outputs
   DevMat scratch_l, scratch_u;  // residual workspaces
   DevMat oneshot;      // one-shot drop-in buffer
+  DevMat batch[2];     // double-buffered device matrices of the pipelined batch API
+  cudaStream_t cin = nullptr, cout = nullptr;  // batch copy streams (H2D, D2H)
   DevMat oneshot_in[4];
   int* info = nullptr;           // device status word
   int* info_host = nullptr;      // pinned mirror(s)
@@ -392,6 +394,83 @@ int oneshot_factor(tt_ctx* ctx, int kernel, double* a, int rows, int cols, int b
   return TT_OK;
 }
 
+// Pipelined batch of one-shot factorisations through host memory: matrix i
+// is uploaded (copy stream), factored (context stream) and downloaded (a
+// second copy stream) while its neighbours are in flight, double-buffered
+// on the device — the host<->device traffic overlaps the factorisations.
+// Host buffers should be page-locked for the copies to be asynchronous.
+int batch_factor(tt_ctx* ctx, int kernel, double* const* mats, int count, int n, int by, int bx,
+                 int* fail_index) {
+  int rc = validate_factor(ctx, kernel, n, n, by, bx);
+  if (rc) return rc;
+  if (count < 0 || (count > 0 && !mats)) return fail(ctx, TT_EINVAL, "batch: bad matrix list");
+  if (eager_mode()) {  // debug aid: no graphs to pipeline, run the one-shot path per matrix
+    for (int i = 0; i < count; ++i) {
+      int idx = -1;
+      rc = oneshot_factor(ctx, kernel, mats[i], n, n, by, bx, &idx);
+      if (fail_index) fail_index[i] = idx;
+      if (rc) return rc;
+    }
+    return TT_OK;
+  }
+  TT_CUDA(ctx, cudaSetDevice(ctx->device), "cudaSetDevice");
+  if (!ctx->cin) TT_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cin, cudaStreamNonBlocking), "stream");
+  if (!ctx->cout) TT_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cout, cudaStreamNonBlocking), "stream");
+  cudaGraphExec_t g[2] = {nullptr, nullptr};
+  long long nodes[2] = {0, 0};
+  for (int b = 0; b < 2 && b < count; ++b) {
+    TT_CUDA(ctx, ensure(ctx->batch[b], n, n), "cudaMalloc");
+    rc = factor_graph(ctx, kernel, ctx->batch[b].p, n, ctx->batch[b].ld, by, bx, &g[b], &nodes[b]);
+    if (rc) return rc;
+  }
+  rc = ensure_info_slots(ctx, std::max(count, 1));
+  if (rc) return rc;
+  std::vector<cudaEvent_t> ev(3 * 2, nullptr);  // per buffer: uploaded, factored, downloaded
+  for (auto& e : ev) TT_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  auto cleanup = [&] {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  };
+  cudaError_t err = cudaSuccess;
+  for (int i = 0; i < count && err == cudaSuccess; ++i) {
+    const int b = i & 1;
+    cudaEvent_t up = ev[3 * b], fac = ev[3 * b + 1], down = ev[3 * b + 2];
+    if (i >= 2) err = cudaStreamWaitEvent(ctx->cin, down, 0);  // buffer b free again
+    if (err == cudaSuccess) err = upload(ctx->batch[b], mats[i], ctx->cin);
+    if (err == cudaSuccess) err = cudaEventRecord(up, ctx->cin);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(ctx->stream, up, 0);
+    if (err == cudaSuccess && g[b]) err = cudaGraphLaunch(g[b], ctx->stream);
+    if (err == cudaSuccess)
+      err = cudaMemcpyAsync(&ctx->info_host[i], ctx->info, sizeof(int), cudaMemcpyDeviceToHost,
+                            ctx->stream);
+    if (err == cudaSuccess) err = cudaEventRecord(fac, ctx->stream);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(ctx->cout, fac, 0);
+    if (err == cudaSuccess) err = download(mats[i], ctx->batch[b], ctx->cout);
+    if (err == cudaSuccess) err = cudaEventRecord(down, ctx->cout);
+    ctx->launches += static_cast<unsigned long long>(nodes[b]);
+  }
+  if (err == cudaSuccess) err = cudaStreamSynchronize(ctx->cout);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(ctx->stream);
+  cleanup();
+  if (err != cudaSuccess) return cuda_fail(ctx, err, "batch factorisation");
+  const int saved = ctx->kernel;
+  ctx->kernel = kernel;
+  for (int i = 0; i < count; ++i) {
+    if (fail_index) fail_index[i] = -1;
+    if (ctx->info_host[i] != tt::kNoFailure) {
+      int idx = -1;
+      rc = numeric_status(ctx, ctx->info_host[i], &idx);
+      if (fail_index) fail_index[i] = idx;
+      if (rc) {
+        ctx->kernel = saved;
+        return rc;  // the first failing matrix decides the status (its index in *fail_index)
+      }
+    }
+  }
+  ctx->kernel = saved;
+  return TT_OK;
+}
+
 double ordered_to_double(unsigned long long u) {
   double d;
   std::memcpy(&d, &u, sizeof d);
@@ -454,8 +533,10 @@ int tt_ctx_destroy(tt_ctx* ctx) {
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
   for (auto& kv : ctx->dag_ws) tt::dag::destroy(&kv.second);
   for (auto* m : {&ctx->work, &ctx->e, &ctx->f, &ctx->g, &ctx->scratch_l, &ctx->scratch_u,
-                  &ctx->oneshot})
+                  &ctx->oneshot, &ctx->batch[0], &ctx->batch[1]})
     release(*m);
+  if (ctx->cin) cudaStreamDestroy(ctx->cin);
+  if (ctx->cout) cudaStreamDestroy(ctx->cout);
   for (auto& m : ctx->pristine) release(m);
   for (auto& m : ctx->oneshot_in) release(m);
   if (ctx->info) cudaFree(ctx->info);
@@ -487,6 +568,18 @@ int tt_cholesky_factor_inplace(tt_ctx* ctx, double* a, int rows, int cols, int b
                                int* fail_index) {
   if (!ctx || !a) return TT_EINVAL;
   return oneshot_factor(ctx, TT_KERNEL_CHOLESKY, a, rows, cols, by, bx, fail_index);
+}
+
+int tt_lu_factor_batch(tt_ctx* ctx, double* const* mats, int count, int n, int by, int bx,
+                       int* fail_index) {
+  if (!ctx) return TT_EINVAL;
+  return batch_factor(ctx, TT_KERNEL_LU, mats, count, n, by, bx, fail_index);
+}
+
+int tt_cholesky_factor_batch(tt_ctx* ctx, double* const* mats, int count, int n, int by, int bx,
+                             int* fail_index) {
+  if (!ctx) return TT_EINVAL;
+  return batch_factor(ctx, TT_KERNEL_CHOLESKY, mats, count, n, by, bx, fail_index);
 }
 
 int tt_mm3_tiled(tt_ctx* ctx, const double* a, const double* b, const double* c,

@@ -126,6 +126,34 @@ def cholesky_factor_inplace(a: np.ndarray, by: int, bx: int, ctx: Context | None
     ctx.check(rc, idx.value)
 
 
+def _factor_batch(fn, mats, by, bx, ctx):
+    mats = [_as_matrix(m) for m in mats]
+    if not mats:
+        return
+    n = mats[0].shape[0]
+    if any(m.shape != (n, n) for m in mats):
+        raise ValueError("batch: all matrices must be square with the same extent")
+    ptrs = (ctypes.c_void_p * len(mats))(*[m.ctypes.data for m in mats])
+    fails = (ctypes.c_int * len(mats))()
+    rc = fn(ctx.handle, ptrs, len(mats), n, int(by), int(bx), fails)
+    first = next((f for f in fails if f >= 0), -1) if rc else None
+    ctx.check(rc, first)
+
+
+def lu_factor_batch(mats, by: int, bx: int, ctx: Context | None = None) -> None:
+    """Pipelined batch of lu_factor_inplace (kernels.hpp:65) over host matrices: the
+    upload / factorisation / download of neighbouring matrices overlap.  Page-locked
+    host buffers (torch pin_memory) give full overlap."""
+    ctx = ctx or default_context()
+    _factor_batch(ctx.lib.tt_lu_factor_batch, mats, by, bx, ctx)
+
+
+def cholesky_factor_batch(mats, by: int, bx: int, ctx: Context | None = None) -> None:
+    """Pipelined batch of cholesky_factor_inplace (kernels.hpp:66)."""
+    ctx = ctx or default_context()
+    _factor_batch(ctx.lib.tt_cholesky_factor_batch, mats, by, bx, ctx)
+
+
 def mm3_tiled(a, b, c, d, config, ctx: Context | None = None) -> np.ndarray:
     """kernels.hpp:43 — G = (A*B)*(C*D) with per-product CTA regions (P0..P5)."""
     a, b, c, d = (_as_matrix(x) for x in (a, b, c, d))

@@ -16,8 +16,8 @@ import pytest
 
 import oracle
 from paper_2309_07235_b200 import (GpuKernelRunner, KernelCase, MeasureProtocol, NumericalError,
-                                   cholesky_factor_inplace, cholesky_tiled, lu_factor_inplace,
-                                   lu_tiled, mm3_tiled)
+                                   cholesky_factor_batch, cholesky_factor_inplace, cholesky_tiled,
+                                   lu_factor_batch, lu_factor_inplace, lu_tiled, mm3_tiled)
 
 pytestmark = pytest.mark.gpu
 
@@ -255,6 +255,38 @@ def test_determinism(gpu_ctx):
     l2, u2 = lu_tiled(a, 8, 6, ctx=gpu_ctx)
     assert np.array_equal(l1, l2) and np.array_equal(u1, u2)
     assert np.array_equal(cholesky_tiled(a, 8, 6, ctx=gpu_ctx), cholesky_tiled(a, 8, 6, ctx=gpu_ctx))
+
+
+def test_batch_api_matches_one_shot(gpu_ctx):
+    """The pipelined batch entry points give, per matrix, exactly the one-shot
+    drop-in's result (same schedule), on pinned and pageable buffers, and report
+    the first failing matrix / column like lu_factor_inplace."""
+    import torch
+    for n, by, bx in ((200, 40, 20), (96, 96, 8), (60, 12, 5)):
+        mats = [oracle.gen_spd(n, s) for s in range(5)]
+        one = [m.copy() for m in mats]
+        for m in one:
+            lu_factor_inplace(m, by, bx, ctx=gpu_ctx)
+        pinned = [torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy() for _ in mats]
+        for p, m in zip(pinned, mats):
+            p[...] = m
+        lu_factor_batch(pinned, by, bx, ctx=gpu_ctx)
+        for p, o in zip(pinned, one):
+            assert np.array_equal(p, o), (n, by, bx)
+        ch = [m.copy() for m in mats]
+        cholesky_factor_batch(ch, by, bx, ctx=gpu_ctx)
+        for c, m in zip(ch, mats):
+            ref = m.copy()
+            cholesky_factor_inplace(ref, by, bx, ctx=gpu_ctx)
+            assert np.array_equal(c, ref)
+    lu_factor_batch([], 1, 1, ctx=gpu_ctx)
+    bad = [oracle.gen_spd(40, 1), np.eye(40), oracle.gen_spd(40, 2)]
+    bad[1][17, 17] = 0.0
+    with pytest.raises(NumericalError) as ei:
+        lu_factor_batch(bad, 40, 8, ctx=gpu_ctx)
+    assert ei.value.index == 17
+    with pytest.raises(ValueError):
+        lu_factor_batch([np.eye(8), np.eye(9)], 1, 1, ctx=gpu_ctx)
 
 
 @pytest.mark.slow
