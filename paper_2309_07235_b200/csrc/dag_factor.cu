@@ -75,6 +75,8 @@ struct Params {
   double* solve;  // per step: 64 reciprocals of the factored diagonal (DIAG -> TRSM)
   int nurgent;    // tasks[0, nurgent): urgent queue; [nurgent, ntasks): bulk queue
   int nuw;        // CTAs 1..nuw serve the urgent queue
+  int pf_mask;    // bit 0: urgent CTAs, bit 1: bulk CTAs fetch the next task before
+                  // the current one's dependency wait (else when warp 0 finishes it)
 };
 
 
@@ -88,21 +90,30 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Acquire load (LDG.STRONG.GPU + L1 invalidate; unlike fence.acq_rel it does
+// not wait for this thread's outstanding loads and stores, so prefetches
+// stay in flight across a dependency check).
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
-// Spins (relaxed gpu-scope loads: no L1 invalidation per poll, with a short
-// back-off so waiting CTAs do not hammer the counter's L2 slice) until
-// *addr >= need, then one acquire fence.  False when the schedule was aborted.
+// Spins (acquire gpu-scope loads, with a short back-off so waiting CTAs do
+// not hammer the counter's L2 slice) until *addr >= need.  False when the
+// schedule was aborted.
 __device__ bool wait_ge(const Params& p, const int* addr, int need) {
-  if (ld_relaxed(addr) < need) {
+  if (ld_acquire(addr) < need) {
     const unsigned long long t0 = globaltimer();
     for (int it = 0;; ++it) {
       __nanosleep(100);
-      if (ld_relaxed(addr) >= need) break;
+      if (ld_acquire(addr) >= need) break;
       if ((it & 15) == 15) {
         if (ld_relaxed(p.abort)) return false;
         if (globaltimer() - t0 > static_cast<unsigned long long>(kWatchdogNs)) {
@@ -113,7 +124,6 @@ __device__ bool wait_ge(const Params& p, const int* addr, int need) {
       }
     }
   }
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
   return true;
 }
 
@@ -181,16 +191,16 @@ __device__ __forceinline__ bool strip_deps(const Params& p, int rs, int re, int 
     if (block) {
       ok = wait_ge(p, c, need);
     } else {
-      ok = ld_relaxed(c) >= need;
-      if (ok) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      ok = ld_acquire(c) >= need;
     }
   }
   return __all_sync(0xffffffffu, ok);
 }
 
-// All lanes of a warp, after storing rows [ra, rb) of tile column j.
+// All lanes of a warp, after storing rows [ra, rb) of tile column j.  The
+// warp barrier orders every lane's stores before lane 0's release reduction
+// (release is cumulative), so no per-lane fence.
 __device__ __forceinline__ void warp_signal(const Params& p, int ra, int rb, int j) {
-  __threadfence();
   __syncwarp();
   if ((threadIdx.x & 31) == 0) {
     for (int i = ra / p.T; i * p.T < rb; ++i) {
@@ -861,22 +871,28 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
     s_task[0] = id < qhi ? p.tasks[id] : kNone;
   }
   __syncthreads();
+  // Early fetch hides the queue atomic behind the dependency wait but binds
+  // the next task to this CTA while the current one may still be waiting on
+  // its inputs (head-of-line blocking); late fetch (warp 0, after its share
+  // of the task) keeps queued tasks free for idle CTAs.
+  const bool early = (p.pf_mask >> (urgent_q ? 0 : 1)) & 1;
   for (int it = 0;; ++it) {
     const int cur = it & 1;
     const int4 tk = s_task[cur];
     if (warp == 0) {
-      // prefetch the next task index; its latency overlaps the dependency wait
       int nid = 0;
       if (lane == 0) {
         if (p.trace) s_t0 = globaltimer();
-        if (tk.x >= 0) nid = qlo + atomicAdd(qnext, 1);
+        if (early && tk.x >= 0) nid = qlo + atomicAdd(qnext, 1);
       }
       const bool ok = tk.x >= 0 && wait_deps<CHOL>(p, tk);
       if (lane == 0) {
         __threadfence();
         s_go = ok;
-        s_id[cur ^ 1] = nid;
-        s_task[cur ^ 1] = (tk.x >= 0 && nid < qhi) ? p.tasks[nid] : kNone;
+        if (early) {
+          s_id[cur ^ 1] = nid;
+          s_task[cur ^ 1] = (tk.x >= 0 && nid < qhi) ? p.tasks[nid] : kNone;
+        }
         if (p.trace) s_t1 = globaltimer();
       }
     }
@@ -982,11 +998,15 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
         for (int c0 = warp * kStrip; c0 < T; c0 += kWarps * kStrip) {
           const int nc = min(kStrip, T - c0);
           warp_trsm<NF>(dk + static_cast<long long>(j - k) * T + c0, 1, ld, nc, T, sm, minv);
-          __threadfence();
           __syncwarp();
           if (lane == 0) red_release_add(&p.cnt[k * nt + j], nc);
         }
       }
+    }
+    if (!early && warp == 0 && lane == 0) {
+      const int nid = qlo + atomicAdd(qnext, 1);
+      s_id[cur ^ 1] = nid;
+      s_task[cur ^ 1] = nid < qhi ? p.tasks[nid] : kNone;
     }
     __syncthreads();  // shared tiles and the task slot are reused next iteration
     if (p.trace && tid == 0) {
@@ -1070,6 +1090,15 @@ int urgent_band() {
     return x >= 1 && x <= 16 ? x : 3;
   }();
   return b;
+}
+
+// TT_DAG_PREFETCH: bit 0 urgent, bit 1 bulk queue CTAs fetch early (default 0: both late).
+int prefetch_mask() {
+  static const int m = [] {
+    const char* v = std::getenv("TT_DAG_PREFETCH");
+    return v ? (std::atoi(v) & 3) : 0;
+  }();
+  return m;
 }
 
 // Two queues, each in step order.  The urgent queue (served by a few
@@ -1185,6 +1214,7 @@ cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long l
   prm.trace = w.trace;
   prm.nurgent = w.nurgent;
   prm.nuw = w.nuw;
+  prm.pf_mask = prefetch_mask();
   prm.solve = w.solve;
   const int nf = (bx + 7) / 8;
   return chol ? launch_nf<true>(nf, prm, w.grid, s) : launch_nf<false>(nf, prm, w.grid, s);

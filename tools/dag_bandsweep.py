@@ -15,4 +15,5 @@ s = r.measure((by, bx), MeasureProtocol(2, 7, "median"))
 fl = (2 / 3 if kern == "lu" else 1 / 3) * n ** 3
 import os
 print(json.dumps({"kernel": kern, "n": n, "by": by, "bx": bx, "band": os.environ.get("TT_DAG_BAND"),
-                  "ucta": os.environ.get("TT_DAG_URGENT_CTAS"), "ms": s * 1e3, "tflops": fl / s / 1e12}))
+                  "ucta": os.environ.get("TT_DAG_URGENT_CTAS"),
+                  "pf": os.environ.get("TT_DAG_PREFETCH"), "ms": s * 1e3, "tflops": fl / s / 1e12}))
