@@ -18,6 +18,7 @@
 // (kernels_test.cpp:284-296).
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 
 #include "dag_factor.cuh"
@@ -257,6 +258,10 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
     }
     cp_async_commit();
   };
+  // C element pairs (2t, 2t+1) as one 16-byte load/store when every row of
+  // the strip starts 16-byte aligned and T is even (half the LSU requests of
+  // 8-byte accesses: the strip's operand round trip is bound by them)
+  const bool cvec = ((reinterpret_cast<uintptr_t>(op.C0) & 15) == 0) && !(op.ldc & 1) && !(T & 1);
   auto load_c = [&](int rs, double (&cv)[kMF][NF][2]) {
     const int nr = min(kStrip, r1 - rs);
 #pragma unroll
@@ -264,19 +269,31 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
       const int r = mf * 8 + g;
       const bool rv = r < nr;
       const double* crow = op.C0 + static_cast<long long>(rs - r0 + (rv ? r : 0)) * op.ldc;
+      if (cvec) {
 #pragma unroll
-      for (int nf = 0; nf < NF; ++nf)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = nf * 8 + 2 * t + h;
-          cv[mf][nf][h] = (op.beta && rv && c < T) ? __ldcg(crow + c) : 0.0;
+        for (int nf = 0; nf < NF; ++nf) {
+          const int c = nf * 8 + 2 * t;
+          double2 v = make_double2(0.0, 0.0);
+          if (op.beta && rv && c < T) v = __ldcg(reinterpret_cast<const double2*>(crow + c));
+          cv[mf][nf][0] = v.x;
+          cv[mf][nf][1] = v.y;
         }
+      } else {
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = nf * 8 + 2 * t + h;
+            cv[mf][nf][h] = (op.beta && rv && c < T) ? __ldcg(crow + c) : 0.0;
+          }
+      }
     }
   };
 
   double acc[kMF][NF][2];
   int prev_ra = -1, prev_nr = 0;
   if (!strip_deps(p, ra, min(ra + kStrip, r1), j, k, op.gemm, true)) return;
+  if (first_done && lane == 0) first_done[2] = globaltimer();  // first strip's inputs final
   issue_a(ra, abuf);
   load_c(ra, acc);
   int cur = 0;
@@ -326,15 +343,18 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
       if (r < nr) {
         double* crow = op.C0 + static_cast<long long>(ra - r0 + r) * op.ldc;
 #pragma unroll
-        for (int nf = 0; nf < NF; ++nf)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = nf * 8 + 2 * t + h;
-            if (c < T && r + lower_off >= c) crow[c] = acc[mf][nf][h];
+        for (int nf = 0; nf < NF; ++nf) {
+          const int c = nf * 8 + 2 * t;
+          const bool ok0 = c < T && r + lower_off >= c, ok1 = c + 1 < T && r + lower_off >= c + 1;
+          if (cvec && ok0 && ok1) {
+            *reinterpret_cast<double2*>(crow + c) = make_double2(acc[mf][nf][0], acc[mf][nf][1]);
+          } else {
+            if (ok0) crow[c] = acc[mf][nf][0];
+            if (ok1) crow[c + 1] = acc[mf][nf][1];
           }
+        }
       }
     }
-    if (first_done && lane == 0) first_done[2] = globaltimer() + static_cast<unsigned long long>(acc[0][0][0] * 0.0);
     prev_ra = ra;
     prev_nr = nr;
     if (first_done && lane == 0) {
@@ -435,8 +455,16 @@ __device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* i
     const double u1 = __shfl_sync(0xffffffffu, v1, kk * 4 + t);
     const double x0 = __shfl_sync(0xffffffffu, w0, kk * 4 + t);
     const double x1 = __shfl_sync(0xffffffffu, w1, kk * 4 + t);
-    const double r = rcp_nr(piv);
-    const double m = g > kk ? agk * r : 0.0;
+    // m = agk / piv off a short chain: MUFU seed r0 (rel. error e ~ 2^-23),
+    // m = agk r0 (1 + e + e^2) (truncation e^3 < 2^-66): 3 dependent DFMAs
+    // after the seed instead of two Newton steps and a multiply.
+    double r0;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(piv));
+    const double e = fma(-piv, r0, 1.0);
+    const double tq = fma(e, e, e);
+    const double m0 = agk * r0;
+    const double m = g > kk ? fma(m0, tq, m0) : 0.0;
+    const double r = fma(r0, tq, r0);
     if (2 * t > kk) v0 = fma(-m, u0, v0);
     if (2 * t + 1 > kk) v1 = fma(-m, u1, v1);
     if (g > kk && 2 * t == kk) v0 = m;
@@ -464,7 +492,7 @@ __device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* i
     for (int ii = 7; ii >= 0; --ii) {
       double acc = ii == c ? 1.0 : 0.0;
 #pragma unroll
-      for (int mm = ii + 1; mm < 8; ++mm) acc = fma(-D[(p + ii) * kNP + p + mm], x[mm], acc);
+      for (int mm = 7; mm > ii; --mm) acc = fma(-D[(p + ii) * kNP + p + mm], x[mm], acc);  // newest last
       x[ii] = acc * (p + ii < T ? rr[ii] : 1.0);
     }
 #pragma unroll
@@ -600,20 +628,34 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
                                           const double* __restrict__ Minv,
                                           const double* __restrict__ msc = nullptr) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  // global row strips: element pairs as 16-byte accesses when aligned
+  const bool vec = !SMEM && cs == 1 && !(rs & 1) && !(T & 1) &&
+                   !(reinterpret_cast<uintptr_t>(base) & 15);
   double ra[NF][kMF][2];
 #pragma unroll
   for (int mf = 0; mf < kMF; ++mf) {
     const int r = mf * 8 + g;
     const bool rv = r < nrows;
     const double* row = base + static_cast<long long>(rv ? r : 0) * rs;
+    if (vec) {
 #pragma unroll
-    for (int b = 0; b < NF; ++b)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = b * 8 + 2 * t + h;
-        const double* src = row + static_cast<long long>(c) * cs;
-        ra[b][mf][h] = (rv && c < T) ? (SMEM ? *src : __ldcg(src)) : 0.0;
+      for (int b = 0; b < NF; ++b) {
+        const int c = b * 8 + 2 * t;
+        double2 v = make_double2(0.0, 0.0);
+        if (rv && c < T) v = __ldcg(reinterpret_cast<const double2*>(row + c));
+        ra[b][mf][0] = v.x;
+        ra[b][mf][1] = v.y;
       }
+    } else {
+#pragma unroll
+      for (int b = 0; b < NF; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = b * 8 + 2 * t + h;
+          const double* src = row + static_cast<long long>(c) * cs;
+          ra[b][mf][h] = (rv && c < T) ? (SMEM ? *src : __ldcg(src)) : 0.0;
+        }
+    }
   }
   // source lanes of the accumulator -> A-fragment relayout inside a quad:
   // A-layout k-step s needs column 4s + t, held by lane (g, 2s + t/2), half t&1.
@@ -660,10 +702,13 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
       const int r = mf * 8 + g;
       if (r < nrows) {
         double* row = base + static_cast<long long>(r) * rs;
+        const int c = b * 8 + 2 * t;
+        if (vec) {
+          if (c < T) *reinterpret_cast<double2*>(row + c) = make_double2(xo[mf][0], xo[mf][1]);
+        } else {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = b * 8 + 2 * t + h;
-          if (c < T) row[static_cast<long long>(c) * cs] = xo[mf][h];
+          for (int h = 0; h < 2; ++h)
+            if (c + h < T) row[static_cast<long long>(c + h) * cs] = xo[mf][h];
         }
       }
     }
@@ -749,19 +794,23 @@ __device__ void walker(const Params& p, double* dsm) {
       __syncthreads();
     }
     stamp(k, 2);
-    diag_blocked<CHOL>(D, T, kT, p.info, inv, rk,
-                       p.trace ? p.trace + 8 * (static_cast<long long>(p.ntasks) + k) + 6 : nullptr);
+    diag_blocked<CHOL>(D, T, kT, p.info, inv, rk);
     stamp(k, 3);
     tile_store<CHOL>(D, dk, ld, T, rk, p.solve + static_cast<long long>(k) * kSolveSlot);
-    __threadfence();
+    // publish: the CTA barrier orders every thread's stores before thread 0's
+    // release reduction (cumulative), so one fence instead of one per warp.
+    // Only warp 0 records failures (factor_block8), so thread 0 sees them.
     __syncthreads();
     if (tid == 0) {
-      if (diag::failed(p.info))
+      const bool f = diag::failed(p.info);
+      s_ok = !f;
+      if (f)
         atomicExch(p.abort, 1);
       else
         red_release_add(&p.cnt[k * nt + k], k >= 1 ? 2 * T : T);  // stage k-1 + DIAG(k)
     }
-    if (diag::failed(p.info)) return;
+    __syncthreads();
+    if (!s_ok) return;
     if (k + 1 >= nt) break;
     // ---- first tiles of the panel: L(k+1,k) = A(k+1,k) U11^-1, U(k,k+1) = L11^-1 A(k,k+1)
     if (!wait1(&p.cnt[(k + 1) * nt + k], kT)) return;
@@ -799,6 +848,7 @@ __device__ void walker(const Params& p, double* dsm) {
       }
     }
     __syncthreads();
+    stamp(k, 6);
     // warps 0..3: L21 strips (X * M = A21); warps 4..7: U12 strips on the
     // transposed view (X * L11^T = A12^T)
     {
@@ -817,6 +867,7 @@ __device__ void walker(const Params& p, double* dsm) {
       }
     }
     __syncthreads();
+    stamp(k, 7);
     {  // publish the solved tiles
       double* gl = p.a + static_cast<long long>(kT + T) * ld + kT;
       double* gu = dk + T;
@@ -826,7 +877,6 @@ __device__ void walker(const Params& p, double* dsm) {
         if (!CHOL) gu[static_cast<long long>(x) * ld + y] = Ut[x * kNP + y];
       }
     }
-    __threadfence();
     __syncthreads();
     if (tid == 0) {
       red_release_add(&p.cnt[(k + 1) * nt + k], T);
@@ -976,7 +1026,7 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
           for (int ii = 7; ii >= 0; --ii) {
             double acc = ii == c ? 1.0 : 0.0;
 #pragma unroll
-            for (int m = ii + 1; m < 8; ++m) acc = fma(-sm[(8 * b + ii) * kNP + 8 * b + m], xr[m], acc);
+            for (int m = 7; m > ii; --m) acc = fma(-sm[(8 * b + ii) * kNP + 8 * b + m], xr[m], acc);
             const int gi = 8 * b + ii;
             xr[ii] = acc * ((unit || gi >= T) ? 1.0 : minv[8 * 64 + gi]);
           }
@@ -1101,6 +1151,31 @@ int prefetch_mask() {
   return m;
 }
 
+// TT_DAG_MERGE="rows,thresh": steps with >= thresh GEMM region-tasks group
+// consecutive row regions into GEMM tasks of >= rows rows (rows 0: off).
+// Default 750,250: measured on B200 over LU N=2000/4000 and Cholesky N=4000
+// (profiles/dag_merge_sweep_r01.txt) — early steps, where the bulk queue is
+// throughput-bound, get 3-6 strips per warp instead of 1-2.
+struct GemmMerge {
+  int rows = 750;
+  long long thresh = 250;
+};
+GemmMerge gemm_merge() {
+  static const GemmMerge g = [] {
+    GemmMerge r;
+    if (const char* v = std::getenv("TT_DAG_MERGE")) {
+      int f = 0;
+      long long t = 0;
+      if (std::sscanf(v, "%d,%lld", &f, &t) >= 1 && f >= 0) {
+        r.rows = f;
+        r.thresh = t;
+      }
+    }
+    return r;
+  }();
+  return g;
+}
+
 // Two queues, each in step order.  The urgent queue (served by a few
 // dedicated CTAs) holds what the walker needs next — per step k: the L21
 // rows of tile row k+2, U(k,k+2), and the GEMM rows of tiles (k+2,k+1),
@@ -1116,6 +1191,7 @@ int prefetch_mask() {
 std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
   const int T = bx, nt = n / bx;
   const int band = urgent_band();
+  const GemmMerge gm = gemm_merge();
   std::vector<int4> urg, bulk;
   bulk.reserve(static_cast<size_t>(count_tasks(chol, n, by, bx)));
   for (int k = 0; k + 1 < nt; ++k) {
@@ -1137,13 +1213,21 @@ std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
     if (!chol)
       for (int j = k + 2; j < nt; ++j) task(kTrsmU, 0, 1, j);
     // row regions outer: a region's GEMMs need only that region's L21 rows
-    // (plus the U12 tiles), so the first GEMMs taken are the first ready
-    for (const auto& rg : reg)
+    // (plus the U12 tiles), so the first GEMMs taken are the first ready.
+    // Steps with many GEMM tasks group `merge` consecutive regions per task
+    // (more strips per warp: the per-task latency is amortised).
+    const int ncols = nt - k - 1, nreg = static_cast<int>(reg.size());
+    const bool merge = gm.rows > 0 && static_cast<long long>(nreg) * ncols >= gm.thresh;
+    for (int g0 = 0, g1; g0 < nreg; g0 = g1) {
+      g1 = g0 + 1;  // regions [g0, g1) form one task: at least gm.rows rows when merging
+      while (merge && g1 < nreg && reg[g1 - 1].second - reg[g0].first < gm.rows) ++g1;
+      const int lo = reg[g0].first, hi = reg[g1 - 1].second;
       for (int j = k + 1; j < nt; ++j) {
-        int r0 = std::max(rg.first, chol ? j * T : pe);  // Cholesky: lower triangle only
-        if (j == k + 1) r0 = std::max(r0, pe + T);        // tile (k+1,k+1): the walker
-        task(kGemm, r0, rg.second, j);
+        int r0 = std::max(lo, chol ? j * T : pe);  // Cholesky: lower triangle only
+        if (j == k + 1) r0 = std::max(r0, pe + T);  // tile (k+1,k+1): the walker
+        task(kGemm, r0, hi, j);
       }
+    }
   }
   if (n_urgent) *n_urgent = static_cast<int>(urg.size());
   urg.insert(urg.end(), bulk.begin(), bulk.end());

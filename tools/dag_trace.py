@@ -25,7 +25,7 @@ nsteps = n // bx
 trall = np.zeros((nt + nsteps, 8), dtype=np.uint64)
 got = ctx.lib.tt_dag_trace(ctx.handle, trall.ctypes.data_as(ctypes.c_void_p), nt + nsteps)
 tr = trall[:nt]
-wk = (trall[nt:, :6].astype(np.int64) - int(tr[:, 0].min())) / 1e3
+wk = (trall[nt:, :8].astype(np.int64) - int(tr[:, 0].min())) / 1e3
 t = tr[:, :3].astype(np.int64)
 t0 = t[:, 0].min()
 t = (t - t0) / 1e3  # us
@@ -45,8 +45,8 @@ print("  walker per step (us): wait tile %.2f, update %.2f, DIAG %.2f, store+wai
     (w[:, 1] - w[:, 0]).mean(), (w[:, 2] - w[:, 1]).mean(), (w[:, 3] - w[:, 2]).mean(),
     (w[:, 4] - w[:, 3]).mean(), (w[:, 5] - w[:, 4]).mean(), np.diff(wk[:, 0]).mean()))
 print("  walker step k=5: " + " ".join("%.1f" % x for x in wk[5]))
-wc = trall[nt + 1:-1, 6:8].astype(np.float64) / 1.96e3  # cycles -> us at 1.96 GHz
-print("  walker DIAG split (us): panels+bar %.2f, factor-next || trailing (+bar) %.2f" % (wc[:, 0].mean(), wc[:, 1].mean()))
+print("  walker L/U split (us): loads+sync %.2f, solves+sync %.2f, publish %.2f" % (
+    (w[:, 6] - w[:, 4]).mean(), (w[:, 7] - w[:, 6]).mean(), (w[:, 5] - w[:, 7]).mean()))
 for kk, nm, a_, b_ in [(2, "TRSM_U", "M load+sync", "8x8 inverses+sync"), (1, "TRSM_L", "M load+sync", "8x8 inverses+sync"), (3, "GEMM", "B load+sync", "first strip (warp 0) done")]:
     mm = kind == kk
     if mm.any():
@@ -54,8 +54,8 @@ for kk, nm, a_, b_ in [(2, "TRSM_U", "M load+sync", "8x8 inverses+sync"), (1, "T
         print(f"  {nm} phases (us after ready): {a_} {(q[:, 0] - t[mm, 1]).mean():.2f}, {b_} +{(q[:, 1] - q[:, 0]).mean():.2f}, end +{(t[mm, 2] - q[:, 1]).mean():.2f}")
 mm = kind == 3
 q = (tr[mm, 4:8].astype(np.int64) - t0) / 1e3
-print("  GEMM first strip (warp 0): data ready +%.2f, computed+stored +%.2f, fence+signal +%.2f us" % (
-    (q[:, 2] - q[:, 0]).mean(), (q[:, 3] - q[:, 2]).mean(), (q[:, 1] - q[:, 3]).mean()))
+print("  GEMM first strip (warp 0) after B: deps +%.2f, loads +%.2f, compute+store +%.2f us" % (
+    (q[:, 3] - q[:, 0]).mean(), (q[:, 2] - q[:, 3]).mean(), (q[:, 1] - q[:, 2]).mean()))
 busy = (t[:, 2] - t[:, 1]).sum()
 grid = len(set(tr[:, 3]))
 print(f"  utilisation (task run time / (SMs x span)) = {busy / (grid * span):.3f}")
