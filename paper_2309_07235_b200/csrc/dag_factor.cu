@@ -415,6 +415,36 @@ constexpr int kPB = 132;  // doubles per parity of the DIAG publication buffer
 template <bool CHOL>
 __device__ __forceinline__ void tile_load(double* D, const double* __restrict__ dk, long long ld,
                                           int T) {
+  if (!(T & 1)) {  // element pairs (16-byte loads); Cholesky mirrors the lower triangle
+    constexpr int kPer = 64 * 32 / kThreads;
+    double2 v[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = threadIdx.x + u * kThreads, i = e >> 5, c = 2 * (e & 31);
+      if (i < T && c < T && (!CHOL || c <= i))
+        v[u] = __ldcg(reinterpret_cast<const double2*>(dk + static_cast<long long>(i) * ld + c));
+      else
+        v[u] = make_double2(i == c ? 1.0 : 0.0, i == c + 1 ? 1.0 : 0.0);
+      if (i >= T || c >= T) v[u] = make_double2(i == c ? 1.0 : 0.0, i == c + 1 ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = threadIdx.x + u * kThreads, i = e >> 5, c = 2 * (e & 31);
+      if (!CHOL) {
+        *reinterpret_cast<double2*>(D + i * kNP + c) = v[u];
+      } else {
+        if (c <= i) {
+          D[i * kNP + c] = v[u].x;
+          D[c * kNP + i] = v[u].x;
+        }
+        if (c + 1 <= i) {
+          D[i * kNP + c + 1] = v[u].y;
+          D[(c + 1) * kNP + i] = v[u].y;
+        }
+      }
+    }
+    return;
+  }
   constexpr int kPer = 64 * 64 / kThreads;
   double v[kPer];
 #pragma unroll
@@ -450,7 +480,9 @@ __device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* i
   for (int kk = 0; kk < 8; ++kk) {
     const double sel = (kk & 1) ? v1 : v0;
     const double piv = __shfl_sync(0xffffffffu, sel, kk * 4 + (kk >> 1));
-    const double agk = __shfl_sync(0xffffffffu, sel, g * 4 + (kk >> 1));
+    // rows above the pivot take a zero multiplier: mask the operand (off the chain)
+    const double agk_all = __shfl_sync(0xffffffffu, sel, g * 4 + (kk >> 1));  // all lanes
+    const double agk = g > kk ? -agk_all : 0.0;
     const double u0 = __shfl_sync(0xffffffffu, v0, kk * 4 + t);
     const double u1 = __shfl_sync(0xffffffffu, v1, kk * 4 + t);
     const double x0 = __shfl_sync(0xffffffffu, w0, kk * 4 + t);
@@ -462,15 +494,15 @@ __device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* i
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(piv));
     const double e = fma(-piv, r0, 1.0);
     const double tq = fma(e, e, e);
-    const double m0 = agk * r0;
-    const double m = g > kk ? fma(m0, tq, m0) : 0.0;
+    const double nm0 = agk * r0;             // -m0 (agk is negated)
+    const double nm = fma(nm0, tq, nm0);     // -m, no select on the chain
     const double r = fma(r0, tq, r0);
-    if (2 * t > kk) v0 = fma(-m, u0, v0);
-    if (2 * t + 1 > kk) v1 = fma(-m, u1, v1);
-    if (g > kk && 2 * t == kk) v0 = m;
-    if (g > kk && 2 * t + 1 == kk) v1 = m;
-    w0 = fma(-m, x0, w0);
-    w1 = fma(-m, x1, w1);
+    if (2 * t > kk) v0 = fma(nm, u0, v0);
+    if (2 * t + 1 > kk) v1 = fma(nm, u1, v1);
+    if (g > kk && 2 * t == kk) v0 = -nm;
+    if (g > kk && 2 * t + 1 == kk) v1 = -nm;
+    w0 = fma(nm, x0, w0);
+    w1 = fma(nm, x1, w1);
     rr[kk] = r;
     // the reference's failure predicates (kernels.cpp:187-190 / :297-302; NaN passes)
     if (p + kk < T && (CHOL ? piv <= 0.0 : fabs(piv) < 1e-300)) fail = min(fail, kk);
@@ -661,32 +693,20 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
   // A-layout k-step s needs column 4s + t, held by lane (g, 2s + t/2), half t&1.
   const int src0 = (lane & ~3) | (t >> 1), src1 = (lane & ~3) | (2 + (t >> 1));
   const bool odd = t & 1;
-  double xa[NF][kMF][2];  // -X in A-fragment layout
+  // Right-looking over the 8-column blocks: once X_b is known it is applied
+  // to every later block's accumulator (R_c -= X_b M_bc), so the serial
+  // chain per block is relayout -> inv(M_bb) DMMA -> relayout -> one update
+  // DMMA pair; the other blocks' updates overlap it.  Each R_c receives the
+  // X_b M_bc terms in ascending b, the same order as the left-looking form.
 #pragma unroll
   for (int b = 0; b < NF; ++b) {
-    double acc[kMF][2];
-#pragma unroll
-    for (int mf = 0; mf < kMF; ++mf) {
-      acc[mf][0] = ra[b][mf][0];
-      acc[mf][1] = ra[b][mf][1];
-    }
-#pragma unroll
-    for (int bb = 0; bb < b; ++bb)
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int mr = bb * 8 + 4 * s + t, mc = b * 8 + g;
-        double m = MMODE == 0 ? Ms[mr * kNP + mc] : Ms[mc * kNP + mr];
-        if (MMODE == 2) m *= msc[mr];
-#pragma unroll
-        for (int mf = 0; mf < kMF; ++mf) dmma_8x8x4(acc[mf][0], acc[mf][1], xa[bb][mf][s], m);
-      }
     double rf[kMF][2];
 #pragma unroll
     for (int mf = 0; mf < kMF; ++mf) {
-      const double v0 = __shfl_sync(0xffffffffu, acc[mf][0], src0);
-      const double v1 = __shfl_sync(0xffffffffu, acc[mf][1], src0);
-      const double w0 = __shfl_sync(0xffffffffu, acc[mf][0], src1);
-      const double w1 = __shfl_sync(0xffffffffu, acc[mf][1], src1);
+      const double v0 = __shfl_sync(0xffffffffu, ra[b][mf][0], src0);
+      const double v1 = __shfl_sync(0xffffffffu, ra[b][mf][1], src0);
+      const double w0 = __shfl_sync(0xffffffffu, ra[b][mf][0], src1);
+      const double w1 = __shfl_sync(0xffffffffu, ra[b][mf][1], src1);
       rf[mf][0] = odd ? v1 : v0;
       rf[mf][1] = odd ? w1 : w0;
     }
@@ -696,6 +716,28 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
       const double m = Minv[b * 64 + (4 * s + t) * 8 + g];
 #pragma unroll
       for (int mf = 0; mf < kMF; ++mf) dmma_8x8x4(xo[mf][0], xo[mf][1], rf[mf][s], m);
+    }
+    if (b + 1 < NF) {
+      double xa[kMF][2];  // -X_b in A-fragment layout
+#pragma unroll
+      for (int mf = 0; mf < kMF; ++mf) {
+        const double v0 = __shfl_sync(0xffffffffu, xo[mf][0], src0);
+        const double v1 = __shfl_sync(0xffffffffu, xo[mf][1], src0);
+        const double w0 = __shfl_sync(0xffffffffu, xo[mf][0], src1);
+        const double w1 = __shfl_sync(0xffffffffu, xo[mf][1], src1);
+        xa[mf][0] = -(odd ? v1 : v0);
+        xa[mf][1] = -(odd ? w1 : w0);
+      }
+#pragma unroll
+      for (int c = b + 1; c < NF; ++c)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int mr = b * 8 + 4 * s + t, mc = c * 8 + g;
+          double m = MMODE == 0 ? Ms[mr * kNP + mc] : Ms[mc * kNP + mr];
+          if (MMODE == 2) m *= msc[mr];
+#pragma unroll
+          for (int mf = 0; mf < kMF; ++mf) dmma_8x8x4(ra[c][mf][0], ra[c][mf][1], xa[mf][s], m);
+        }
     }
 #pragma unroll
     for (int mf = 0; mf < kMF; ++mf) {
@@ -710,17 +752,6 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
           for (int h = 0; h < 2; ++h)
             if (c + h < T) row[static_cast<long long>(c + h) * cs] = xo[mf][h];
         }
-      }
-    }
-    if (b + 1 < NF) {
-#pragma unroll
-      for (int mf = 0; mf < kMF; ++mf) {
-        const double v0 = __shfl_sync(0xffffffffu, xo[mf][0], src0);
-        const double v1 = __shfl_sync(0xffffffffu, xo[mf][1], src0);
-        const double w0 = __shfl_sync(0xffffffffu, xo[mf][0], src1);
-        const double w1 = __shfl_sync(0xffffffffu, xo[mf][1], src1);
-        xa[b][mf][0] = -(odd ? v1 : v0);
-        xa[b][mf][1] = -(odd ? w1 : w0);
       }
     }
   }
@@ -819,14 +850,26 @@ __device__ void walker(const Params& p, double* dsm) {
     {
       const double* al = p.a + static_cast<long long>(kT + T) * ld + kT;
       const double* au = dk + T;
-      constexpr int kPer = (Tp * Tp + kThreads - 1) / kThreads;
-      double vl[kPer], vu[kPer];
+      // element pairs (16-byte loads; T even keeps every pair aligned, T odd
+      // loads the odd tail element alone)
+      constexpr int kHP = Tp / 2, kPer = (Tp * kHP + kThreads - 1) / kThreads;
+      double2 vl[kPer], vu[kPer];
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
-        const int e = tid + u * kThreads, x = e / Tp, y = e - x * Tp;
-        const bool in = e < Tp * Tp && x < T && y < T;
-        vl[u] = in ? __ldcg(al + static_cast<long long>(x) * ld + y) : 0.0;
-        vu[u] = (!CHOL && in) ? __ldcg(au + static_cast<long long>(x) * ld + y) : 0.0;
+        const int e = tid + u * kThreads, x = e / kHP, y = 2 * (e - x * kHP);
+        const bool in = e < Tp * kHP && x < T && y < T;
+        vl[u] = vu[u] = make_double2(0.0, 0.0);
+        if (in && !(T & 1)) {
+          vl[u] = __ldcg(reinterpret_cast<const double2*>(al + static_cast<long long>(x) * ld + y));
+          if (!CHOL) vu[u] = __ldcg(reinterpret_cast<const double2*>(au + static_cast<long long>(x) * ld + y));
+        } else if (in) {
+          vl[u].x = __ldcg(al + static_cast<long long>(x) * ld + y);
+          if (y + 1 < T) vl[u].y = __ldcg(al + static_cast<long long>(x) * ld + y + 1);
+          if (!CHOL) {
+            vu[u].x = __ldcg(au + static_cast<long long>(x) * ld + y);
+            if (y + 1 < T) vu[u].y = __ldcg(au + static_cast<long long>(x) * ld + y + 1);
+          }
+        }
       }
       // the solves read M straight from the factored tile D: U11 = upper(D),
       // L11^T = lower(D)^T (Cholesky scaled by l_kk); only strictly-upper
@@ -840,10 +883,10 @@ __device__ void walker(const Params& p, double* dsm) {
       }
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
-        const int e = tid + u * kThreads, x = e / Tp, y = e - x * Tp;
-        if (e < Tp * Tp) {
-          Lt[x * kNP + y] = vl[u];
-          if (!CHOL) Ut[x * kNP + y] = vu[u];
+        const int e = tid + u * kThreads, x = e / kHP, y = 2 * (e - x * kHP);
+        if (e < Tp * kHP) {
+          *reinterpret_cast<double2*>(Lt + x * kNP + y) = vl[u];
+          if (!CHOL) *reinterpret_cast<double2*>(Ut + x * kNP + y) = vu[u];
         }
       }
     }
@@ -871,10 +914,24 @@ __device__ void walker(const Params& p, double* dsm) {
     {  // publish the solved tiles
       double* gl = p.a + static_cast<long long>(kT + T) * ld + kT;
       double* gu = dk + T;
-      for (int e = tid; e < T * T; e += kThreads) {
-        const int x = e / T, y = e - x * T;
-        gl[static_cast<long long>(x) * ld + y] = Lt[x * kNP + y];
-        if (!CHOL) gu[static_cast<long long>(x) * ld + y] = Ut[x * kNP + y];
+      if (!(T & 1)) {  // 16-byte stores of element pairs
+        constexpr int kHP = Tp / 2;
+        for (int e = tid; e < Tp * kHP; e += kThreads) {
+          const int x = e / kHP, y = 2 * (e - x * kHP);
+          if (x < T && y < T) {
+            *reinterpret_cast<double2*>(gl + static_cast<long long>(x) * ld + y) =
+                *reinterpret_cast<const double2*>(Lt + x * kNP + y);
+            if (!CHOL)
+              *reinterpret_cast<double2*>(gu + static_cast<long long>(x) * ld + y) =
+                  *reinterpret_cast<const double2*>(Ut + x * kNP + y);
+          }
+        }
+      } else {
+        for (int e = tid; e < T * T; e += kThreads) {
+          const int x = e / T, y = e - x * T;
+          gl[static_cast<long long>(x) * ld + y] = Lt[x * kNP + y];
+          if (!CHOL) gu[static_cast<long long>(x) * ld + y] = Ut[x * kNP + y];
+        }
       }
     }
     __syncthreads();
