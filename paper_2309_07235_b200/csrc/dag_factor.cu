@@ -472,8 +472,6 @@ __device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* i
   double* invL = inv + 512 + b * 64;
   __syncwarp();  // converged warp: keeps the shuffles on the fast path
   double v0 = D[(p + g) * kNP + p + 2 * t], v1 = D[(p + g) * kNP + p + 2 * t + 1];
-  // W = I, transformed by the same row operations: ends as inv(L_bb)
-  double w0 = g == 2 * t ? 1.0 : 0.0, w1 = g == 2 * t + 1 ? 1.0 : 0.0;
   double rr[8];
   int fail = INT_MAX;  // first failing pivot (warp-uniform: pivots come by shuffle)
 #pragma unroll
@@ -485,8 +483,6 @@ __device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* i
     const double agk = g > kk ? -agk_all : 0.0;
     const double u0 = __shfl_sync(0xffffffffu, v0, kk * 4 + t);
     const double u1 = __shfl_sync(0xffffffffu, v1, kk * 4 + t);
-    const double x0 = __shfl_sync(0xffffffffu, w0, kk * 4 + t);
-    const double x1 = __shfl_sync(0xffffffffu, w1, kk * 4 + t);
     // m = agk / piv off a short chain: MUFU seed r0 (rel. error e ~ 2^-23),
     // m = agk r0 (1 + e + e^2) (truncation e^3 < 2^-66): 3 dependent DFMAs
     // after the seed instead of two Newton steps and a multiply.
@@ -501,34 +497,49 @@ __device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* i
     if (2 * t + 1 > kk) v1 = fma(nm, u1, v1);
     if (g > kk && 2 * t == kk) v0 = -nm;
     if (g > kk && 2 * t + 1 == kk) v1 = -nm;
-    w0 = fma(nm, x0, w0);
-    w1 = fma(nm, x1, w1);
     rr[kk] = r;
     // the reference's failure predicates (kernels.cpp:187-190 / :297-302; NaN passes)
     if (p + kk < T && (CHOL ? piv <= 0.0 : fabs(piv) < 1e-300)) fail = min(fail, kk);
   }
   D[(p + g) * kNP + p + 2 * t] = v0;
   D[(p + g) * kNP + p + 2 * t + 1] = v1;
-  invL[g * 8 + 2 * t] = w0;
-  invL[g * 8 + 2 * t + 1] = w1;
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk)
     if (p + kk < T) rk[p + kk] = rr[kk];  // same value from every lane
   if (fail != INT_MAX && lane == 0) atomicMin(info, gcol + p + fail);
   __syncwarp();
-  // inv(U_bb): lanes 0..7 (column c, back substitution, no divisions)
-  if (lane < 8) {
-    const int c = lane;
+  // inv(U_bb) (lanes 0..7) and inv(L_bb) (lanes 8..15), one column per lane,
+  // by back substitution without divisions.  Both run the same instruction
+  // stream: lanes 8..15 read the unit lower L through its reversal J L J
+  // (upper; staged in `rev`), whose inverse is J inv(L) J.  (Keeping inv(L)
+  // out of the pivot loop saves two double shuffles per pivot.)
+  double* rev = invL;  // the 8x8 reversal, overwritten by inv(L) below
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int col = 2 * t + h;
+    if (g > col) rev[(7 - g) * 8 + 7 - col] = h ? v1 : v0;  // strict upper part of J L J
+  }
+  __syncwarp();
+  if (lane < 16) {
+    const bool lo = lane >= 8;
+    const int c = lane & 7;
+    const double* m = lo ? rev : D + p * kNP + p;
+    const int ms = lo ? 8 : kNP;
     double x[8];
 #pragma unroll
     for (int ii = 7; ii >= 0; --ii) {
       double acc = ii == c ? 1.0 : 0.0;
 #pragma unroll
-      for (int mm = 7; mm > ii; --mm) acc = fma(-D[(p + ii) * kNP + p + mm], x[mm], acc);  // newest last
-      x[ii] = acc * (p + ii < T ? rr[ii] : 1.0);
+      for (int mm = 7; mm > ii; --mm) acc = fma(-m[ii * ms + mm], x[mm], acc);  // newest term last
+      x[ii] = lo ? acc : acc * (p + ii < T ? rr[ii] : 1.0);
     }
+    __syncwarp(0x0000ffffu);  // all reads of `rev` done before inv(L) overwrites it
+    double* dst = lo ? invL : invU;
 #pragma unroll
-    for (int ii = 0; ii < 8; ++ii) invU[ii * 8 + c] = x[ii];
+    for (int ii = 0; ii < 8; ++ii) {
+      const int r = lo ? 7 - ii : ii, cc = lo ? 7 - c : c;
+      dst[r * 8 + cc] = x[ii];
+    }
   }
 }
 
@@ -609,7 +620,12 @@ __device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* in
       __syncwarp();
       factor_block8<CHOL>(D, T, gcol, info, inv, rk, b + 1);
     } else {  // the rest of step b's trailing update
-      for (int ir = warp - 1; ir < nr; ir += kWarps - 1) trail_row(D, b, nr, ir, ir == 0 ? 1 : 0);
+      // warps 1-3, 5-7 only: warp 4 shares warp 0's SM sub-partition (and its
+      // fp64 pipe), where its DMMAs would stall warp 0's DFMA chain
+      if (warp != 4) {
+        const int wi = warp < 4 ? warp - 1 : warp - 2;
+        for (int ir = wi; ir < nr; ir += kWarps - 2) trail_row(D, b, nr, ir, ir == 0 ? 1 : 0);
+      }
     }
     if (prof && tid == 0) c_panel += c2 - c1;
     __syncthreads();
