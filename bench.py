@@ -330,10 +330,9 @@ def run_gpu_arm(args, rank, world, local):
                                        ctypes.byref(idx)))  # warm the one-shot graph
     ptrs = (ctypes.c_void_p * e2e_steps)(*[h.ctypes.data for h in host[:e2e_steps]])
     fails = (ctypes.c_int * e2e_steps)()
-    for h in host[:2]:
-        h[...] = host_a
-    ctx.check(lib.tt_lu_factor_batch(ctx.handle, ptrs, 2, n, by, bx, fails))  # warm the batch graphs
-    for h in host[:2]:
+    # warm-up: the same batch call as the timed one (graphs, streams, status slots)
+    ctx.check(lib.tt_lu_factor_batch(ctx.handle, ptrs, e2e_steps, n, by, bx, fails))
+    for h in host[:e2e_steps]:
         h[...] = host_a
     barrier(world)
     t0 = time.perf_counter()

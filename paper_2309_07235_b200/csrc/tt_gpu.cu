@@ -182,6 +182,9 @@ int validate_mm3(tt_ctx* ctx, int n, int l, int m, int o, int p, const int* cfg,
 
 int ensure_info_slots(tt_ctx* ctx, int slots) {
   if (ctx->info_host_slots >= slots) return TT_OK;
+  // grow geometrically (>= 256 slots): cudaFreeHost synchronises the device
+  // and page-locking is slow, so a batch call must not hit this every time
+  slots = std::max({slots, 256, 2 * ctx->info_host_slots});
   if (ctx->info_host) cudaFreeHost(ctx->info_host);
   ctx->info_host = nullptr;
   TT_CUDA(ctx, cudaMallocHost(&ctx->info_host, sizeof(int) * slots), "cudaMallocHost");
