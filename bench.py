@@ -47,7 +47,7 @@ sys.path.insert(0, str(ROOT))
 FP64_PEAK_TFLOPS = 37.05  # measured DMMA m8n8k4 issue rate (profiles/fp64_peak_r01.jsonl)
 FP64_PEAK_SOURCE = "measured: DMMA issue-rate microbenchmark, 148 SMs @1965 MHz (profiles/fp64_peak_r01.jsonl); cuBLAS DGEMM 8192^3 = 35.45"
 BENCH_N = 2000
-BENCH_LU_BLOCK = (250, 50)  # (by, bx): fastest fixed block of the N=2000 knob sweep (profiles/sweep_lu2000_r01.jsonl); the paper's A100 best was (400, 50)
+BENCH_LU_BLOCK = (200, 40)  # (by, bx): fastest fixed block of the N=2000 knob sweep of the final round-1 kernel (profiles/sweep_lu2000_r01c.jsonl: 0.879 ms; (250,50) 0.930, the paper's A100 best (400,50) 1.000)
 METRIC = "fp64 GFLOP/s of best-tuned config (% of B200 fp64 peak); tuning time-to-best"
 
 
