@@ -165,3 +165,26 @@ def test_measured_tune_on_gpu(tmp_path):
     recs = [l.split(",") for l in text.splitlines() if not l.startswith("#")]
     assert len(recs) == 8 and all(r[6] == "0" and r[7] in ("dag", "graph") for r in recs)
     assert "best_runtime_s:" in p.stdout
+
+
+@pytest.mark.gpu
+def test_measured_tune_two_workers_trace_invariants(tmp_path):
+    """--batch 2 on one GPU: two concurrent evaluators (two contexts on device 0);
+    records in completion order keep elapsed non-decreasing and best_so_far an
+    exact prefix-min (harness_test.cpp:133-153), and both workers report."""
+    out = tmp_path / "b2.trace"
+    run("tune", "3mm", "small", "--tuner", "random", "--max-evals", 12, "--gpus", 1, "--batch", 2,
+        "--seed", 5, "--out", out, env={"TILETUNER_REPS": "1"}, check_rc=0)
+    text = out.read_text()
+    assert "# batch: 2" in text and "# devices: 0,0" in text
+    recs = [l.split(",") for l in text.splitlines() if not l.startswith("#")]
+    assert len(recs) == 12 and all(r[7] == "dgemm" for r in recs)
+    el = [float(r[3]) for r in recs]
+    assert el == sorted(el)
+    best, prefix = float("inf"), []
+    for r in recs:
+        if r[5] == "ok":
+            best = min(best, float(r[2]))
+        prefix.append(best)
+    assert [float(r[4]) for r in recs] == prefix
+    assert sorted(int(r[0]) for r in recs) == list(range(12))
