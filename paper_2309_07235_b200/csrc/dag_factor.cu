@@ -1033,7 +1033,29 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
       // B = U(k, j) (LU) or L(j, k)^T (Cholesky), zero-padded to Tp x Tp
       const double* bsrc = CHOL ? p.a + static_cast<long long>(j * T) * ld + kT
                                 : p.a + static_cast<long long>(kT) * ld + j * T;
-      {  // all loads in flight before any store: one L2 round trip
+      if (!(T & 1)) {  // element pairs, 16-byte loads; all in flight before any store
+        constexpr int kHP = Tp / 2, kPer = (Tp * kHP + kThreads - 1) / kThreads;
+        double2 v[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int e = tid + u * kThreads, x = e / kHP, y = 2 * (e - x * kHP);  // x: slow index
+          v[u] = (e < Tp * kHP && x < T && y < T)
+                     ? __ldcg(reinterpret_cast<const double2*>(bsrc + static_cast<long long>(x) * ld + y))
+                     : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int e = tid + u * kThreads, x = e / kHP, y = 2 * (e - x * kHP);
+          if (e < Tp * kHP) {
+            if (CHOL) {  // B[k][n] = L[n][k]
+              sm[y * kNP + x] = v[u].x;
+              sm[(y + 1) * kNP + x] = v[u].y;
+            } else {
+              *reinterpret_cast<double2*>(sm + x * kNP + y) = v[u];
+            }
+          }
+        }
+      } else {  // all loads in flight before any store: one L2 round trip
         constexpr int kPer = (Tp * Tp + kThreads - 1) / kThreads;
         double v[kPer];
 #pragma unroll
