@@ -1170,8 +1170,21 @@ cudaError_t launch(const Params& prm, int grid, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dag_kernel<NF, CHOL><<<grid, kThreads, kSmemBytes, s>>>(prm);
-  return cudaGetLastError();
+  // Cooperative launch: all CTAs are co-resident before any runs.  The CTAs
+  // spin on each other's counters, so a partially resident grid (another
+  // context's persistent kernel holding SMs, e.g. two tuning workers on one
+  // GPU) could otherwise wait on tasks no resident CTA serves.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, dag_kernel<NF, CHOL>, prm);
 }
 
 template <bool CHOL>

@@ -188,3 +188,15 @@ def test_measured_tune_two_workers_trace_invariants(tmp_path):
         prefix.append(best)
     assert [float(r[4]) for r in recs] == prefix
     assert sorted(int(r[0]) for r in recs) == list(range(12))
+
+
+@pytest.mark.gpu
+def test_two_workers_one_gpu_persistent_factorisations(tmp_path):
+    """Two evaluators on one GPU run persistent (spin-waiting) factorisation
+    kernels concurrently: cooperative launches keep each grid co-resident, so
+    neither waits on CTAs that cannot be scheduled (no watchdog abort)."""
+    out = tmp_path / "lu2.trace"
+    run("tune", "lu", "small", "--tuner", "random", "--max-evals", 10, "--gpus", 1, "--batch", 2,
+        "--seed", 3, "--out", out, env={"TILETUNER_REPS": "2"}, check_rc=0)
+    recs = [l.split(",") for l in out.read_text().splitlines() if not l.startswith("#")]
+    assert len(recs) == 10 and all(r[5] == "ok" for r in recs)
