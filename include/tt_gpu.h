@@ -77,8 +77,8 @@ int tt_cholesky_factor_inplace(tt_ctx* ctx, double* a, int rows, int cols,
                                int by, int bx, int* fail_index);
 /* Pipelined batches of the two drop-ins: `count` row-major n x n host
  * matrices (page-locked for full overlap), each factored in place; upload,
- * factorisation and download of neighbouring matrices overlap (double-
- * buffered on the device).  fail_index (count entries, may be NULL) gets
+ * factorisation and download of neighbouring matrices overlap (three
+ * device buffers).  fail_index (count entries, may be NULL) gets
  * each matrix's failing column or -1; the status is that of the first
  * failing matrix. */
 int tt_lu_factor_batch(tt_ctx* ctx, double* const* mats, int count, int n,

@@ -63,7 +63,7 @@ struct tt_ctx {
   DevMat e, f, g;      // mm3 outputs
   DevMat scratch_l, scratch_u;  // residual workspaces
   DevMat oneshot;      // one-shot drop-in buffer
-  DevMat batch[2];     // double-buffered device matrices of the pipelined batch API
+  DevMat batch[3];     // triple-buffered device matrices of the pipelined batch API
   cudaStream_t cin = nullptr, cout = nullptr;  // batch copy streams (H2D, D2H)
   DevMat oneshot_in[4];
   int* info = nullptr;           // device status word
@@ -399,7 +399,7 @@ int oneshot_factor(tt_ctx* ctx, int kernel, double* a, int rows, int cols, int b
 
 // Pipelined batch of one-shot factorisations through host memory: matrix i
 // is uploaded (copy stream), factored (context stream) and downloaded (a
-// second copy stream) while its neighbours are in flight, double-buffered
+// second copy stream) while its neighbours are in flight, triple-buffered
 // on the device — the host<->device traffic overlaps the factorisations.
 // Host buffers should be page-locked for the copies to be asynchronous.
 int batch_factor(tt_ctx* ctx, int kernel, double* const* mats, int count, int n, int by, int bx,
@@ -419,16 +419,22 @@ int batch_factor(tt_ctx* ctx, int kernel, double* const* mats, int count, int n,
   TT_CUDA(ctx, cudaSetDevice(ctx->device), "cudaSetDevice");
   if (!ctx->cin) TT_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cin, cudaStreamNonBlocking), "stream");
   if (!ctx->cout) TT_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cout, cudaStreamNonBlocking), "stream");
-  cudaGraphExec_t g[2] = {nullptr, nullptr};
-  long long nodes[2] = {0, 0};
-  for (int b = 0; b < 2 && b < count; ++b) {
+  // Three device buffers: a buffer is re-uploaded only after its previous
+  // matrix was downloaded, so with two the upload and download of one buffer
+  // would sit between its factorisations (measured 1.07 ms per matrix at
+  // N=2000 against 0.88 ms for the kernel); with three the copies of the
+  // other buffers run while one factorises.
+  constexpr int kBufs = 3;
+  cudaGraphExec_t g[kBufs] = {};
+  long long nodes[kBufs] = {};
+  for (int b = 0; b < kBufs && b < count; ++b) {
     TT_CUDA(ctx, ensure(ctx->batch[b], n, n), "cudaMalloc");
     rc = factor_graph(ctx, kernel, ctx->batch[b].p, n, ctx->batch[b].ld, by, bx, &g[b], &nodes[b]);
     if (rc) return rc;
   }
   rc = ensure_info_slots(ctx, std::max(count, 1));
   if (rc) return rc;
-  std::vector<cudaEvent_t> ev(3 * 2, nullptr);  // per buffer: uploaded, factored, downloaded
+  std::vector<cudaEvent_t> ev(3 * kBufs, nullptr);  // per buffer: uploaded, factored, downloaded
   for (auto& e : ev) TT_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   auto cleanup = [&] {
     for (auto& e : ev)
@@ -436,9 +442,9 @@ int batch_factor(tt_ctx* ctx, int kernel, double* const* mats, int count, int n,
   };
   cudaError_t err = cudaSuccess;
   for (int i = 0; i < count && err == cudaSuccess; ++i) {
-    const int b = i & 1;
+    const int b = i % kBufs;
     cudaEvent_t up = ev[3 * b], fac = ev[3 * b + 1], down = ev[3 * b + 2];
-    if (i >= 2) err = cudaStreamWaitEvent(ctx->cin, down, 0);  // buffer b free again
+    if (i >= kBufs) err = cudaStreamWaitEvent(ctx->cin, down, 0);  // buffer b free again
     if (err == cudaSuccess) err = upload(ctx->batch[b], mats[i], ctx->cin);
     if (err == cudaSuccess) err = cudaEventRecord(up, ctx->cin);
     if (err == cudaSuccess) err = cudaStreamWaitEvent(ctx->stream, up, 0);
@@ -536,7 +542,7 @@ int tt_ctx_destroy(tt_ctx* ctx) {
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
   for (auto& kv : ctx->dag_ws) tt::dag::destroy(&kv.second);
   for (auto* m : {&ctx->work, &ctx->e, &ctx->f, &ctx->g, &ctx->scratch_l, &ctx->scratch_u,
-                  &ctx->oneshot, &ctx->batch[0], &ctx->batch[1]})
+                  &ctx->oneshot, &ctx->batch[0], &ctx->batch[1], &ctx->batch[2]})
     release(*m);
   if (ctx->cin) cudaStreamDestroy(ctx->cin);
   if (ctx->cout) cudaStreamDestroy(ctx->cout);
