@@ -76,6 +76,7 @@ struct Params {
   double* solve;  // per step: 64 reciprocals of the factored diagonal (DIAG -> TRSM)
   int nurgent;    // tasks[0, nurgent): urgent queue; [nurgent, ntasks): bulk queue
   int nuw;        // CTAs 1..nuw serve the urgent queue
+  int eager_sig;  // publish each GEMM strip right after its stores
   int pf_mask;    // bit 0: urgent CTAs, bit 1: bulk CTAs fetch the next task before
                   // the current one's dependency wait (else when warp 0 finishes it)
 };
@@ -335,7 +336,7 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
     }
     // publish the previous strip now: its stores were issued a whole strip
     // ago, so the fence does not stall on their acknowledgement
-    if (prev_ra >= 0) warp_signal(p, prev_ra, prev_ra + prev_nr, j);
+    if (prev_ra >= 0 && !p.eager_sig) warp_signal(p, prev_ra, prev_ra + prev_nr, j);
     const int lower_off = chol ? ra - jT : kNoLower;
 #pragma unroll
     for (int mf = 0; mf < kMF; ++mf) {
@@ -355,8 +356,13 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
         }
       }
     }
-    prev_ra = ra;
-    prev_nr = nr;
+    if (p.eager_sig) {
+      warp_signal(p, ra, ra + nr, j);  // publish this strip right away
+      prev_ra = -1;
+    } else {
+      prev_ra = ra;
+      prev_nr = nr;
+    }
     if (first_done && lane == 0) {
       *first_done = globaltimer();
       first_done = nullptr;
@@ -1397,6 +1403,12 @@ cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long l
   prm.nurgent = w.nurgent;
   prm.nuw = w.nuw;
   prm.pf_mask = prefetch_mask();
+  // measured default: Cholesky (whose bulk GEMMs feed the next step's strips
+  // directly) gains 2% from publishing each strip at once, LU does not
+  prm.eager_sig = [chol] {
+    const char* v = std::getenv("TT_DAG_EAGER_SIGNAL");
+    return v ? std::atoi(v) : (chol ? 1 : 0);
+  }();
   prm.solve = w.solve;
   const int nf = (bx + 7) / 8;
   return chol ? launch_nf<true>(nf, prm, w.grid, s) : launch_nf<false>(nf, prm, w.grid, s);
