@@ -76,7 +76,7 @@ struct Params {
   double* solve;  // per step: 64 reciprocals of the factored diagonal (DIAG -> TRSM)
   int nurgent;    // tasks[0, nurgent): urgent queue; [nurgent, ntasks): bulk queue
   int nuw;        // CTAs 1..nuw serve the urgent queue
-  int eager_sig;  // publish each GEMM strip right after its stores
+  int eager_sig;  // publish GEMM strips right after their stores: 0 no, 1 all, 2 urgent, 3 bulk
   int pf_mask;    // bit 0: urgent CTAs, bit 1: bulk CTAs fetch the next task before
                   // the current one's dependency wait (else when warp 0 finishes it)
 };
@@ -234,6 +234,7 @@ struct StripOps {
   int cj;      // tile column of C (counters)
   bool gemm;   // also wait for L(i,k) final
   bool beta;   // load C
+  bool eager;  // publish each strip right after its stores (else one strip later)
 };
 
 template <int NF>
@@ -336,7 +337,7 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
     }
     // publish the previous strip now: its stores were issued a whole strip
     // ago, so the fence does not stall on their acknowledgement
-    if (prev_ra >= 0 && !p.eager_sig) warp_signal(p, prev_ra, prev_ra + prev_nr, j);
+    if (prev_ra >= 0 && !op.eager) warp_signal(p, prev_ra, prev_ra + prev_nr, j);
     const int lower_off = chol ? ra - jT : kNoLower;
 #pragma unroll
     for (int mf = 0; mf < kMF; ++mf) {
@@ -356,7 +357,7 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
         }
       }
     }
-    if (p.eager_sig) {
+    if (op.eager) {
       warp_signal(p, ra, ra + nr, j);  // publish this strip right away
       prev_ra = -1;
     } else {
@@ -1081,6 +1082,8 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
       op.cj = j;
       op.gemm = true;
       op.beta = true;
+      // p.eager_sig: 0 none, 1 all GEMM tasks, 2 urgent-queue CTAs only, 3 bulk only
+      op.eager = p.eager_sig == 1 || (p.eager_sig == 2 && urgent_q) || (p.eager_sig == 3 && !urgent_q);
       gemm_strips<NF>(p, r0, r1, k, op, sm, abuf + warp * 2 * kABuf, CHOL,
                       (p.trace && warp == 0) ? &s_ph[1] : nullptr);
     } else {  // TRSM
