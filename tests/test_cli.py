@@ -121,6 +121,22 @@ def test_v1_reader_accepts_reference_format_and_rejects_bad(tmp_path):
     assert run("show", bad).returncode == 1
 
 
+@pytest.mark.parametrize("name,evals,best", [
+    ("tune_lu_large_bo60_r01c.trace", 60, "P0=200|P1=40"),
+    ("tune_chol_xl_bo60_r01c.trace", 60, "P0=250|P1=50"),
+    ("tune_3mm_xl_bo200_r01c.trace", 200, None)])
+def test_reads_measured_v2_traces_from_the_gpu(name, evals, best):
+    """The committed traces of measured GPU runs (profiles/) parse back: v2
+    header, device and schedule-variant columns, best record."""
+    path = ROOT / "profiles" / name
+    out = run("show", path, check_rc=0).stdout
+    assert "version: v2" in out and f"evals: {evals}" in out and "devices_used: 0" in out
+    if best:
+        assert f"best_config: {best}" in out
+    variants = {l.split(",")[7] for l in path.read_text().splitlines() if not l.startswith("#")}
+    assert variants <= {"dag", "graph", "dgemm"} and variants
+
+
 def test_synthetic_batch_and_reproducible(tmp_path):
     a, b = tmp_path / "a.trace", tmp_path / "b.trace"
     for f in (a, b):
