@@ -22,6 +22,7 @@
 #include <cstdlib>
 
 #include "dag_factor.cuh"
+#include "devattr.hpp"
 #include "diag_factor.cuh"
 #include "tt_ptx.cuh"
 
@@ -392,9 +393,23 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
 // division sequence) — the pivot reciprocal sits on the factorisation's
 // serial chain.  Within 1 ulp of 1/x for the normal pivots that pass the
 // reference's failure checks.
-__device__ __forceinline__ double rcp_nr(double x) {
+// MUFU reciprocal seed.  rcp.approx.ftz.f64 flushes results below 2^-1022
+// to zero, i.e. every |x| > 2^1022 would get r = 0 (and a zero multiplier,
+// where the reference divides exactly, kernels.cpp:191): such pivots (a
+// warp-uniform, never-taken-in-practice branch) take the seed of x/4, scaled
+// back by 1/4 — a subnormal reciprocal with >= 50 significant bits.
+__device__ __forceinline__ double rcp_seed(double x) {
   double r;
+  if (fabs(x) > 0x1p1021) {
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x * 0.25));
+    return r * 0.25;
+  }
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r = rcp_seed(x);
   double e = fma(-x, r, 1.0);
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
@@ -493,8 +508,7 @@ __device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* i
     // m = agk / piv off a short chain: MUFU seed r0 (rel. error e ~ 2^-23),
     // m = agk r0 (1 + e + e^2) (truncation e^3 < 2^-66): 3 dependent DFMAs
     // after the seed instead of two Newton steps and a multiply.
-    double r0;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(piv));
+    const double r0 = rcp_seed(piv);
     const double e = fma(-piv, r0, 1.0);
     const double tq = fma(e, e, e);
     const double nm0 = agk * r0;             // -m0 (agk is negated)
@@ -1170,15 +1184,15 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
 }
 
 template <int NF, bool CHOL>
+cudaError_t optin() {
+  static std::atomic<unsigned long long> configured{0};  // one bit per device
+  return smem_optin(dag_kernel<NF, CHOL>, kSmemBytes, configured);
+}
+
+template <int NF, bool CHOL>
 cudaError_t launch(const Params& prm, int grid, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(dag_kernel<NF, CHOL>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               kSmemBytes);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  const cudaError_t e = optin<NF, CHOL>();
+  if (e != cudaSuccess) return e;
   // Cooperative launch: all CTAs are co-resident before any runs.  The CTAs
   // spin on each other's counters, so a partially resident grid (another
   // context's persistent kernel holding SMs, e.g. two tuning workers on one
@@ -1211,6 +1225,19 @@ cudaError_t launch_nf(int nf, const Params& prm, int grid, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
+template <bool CHOL>
+cudaError_t optin_all() {
+  cudaError_t e = optin<1, CHOL>();
+  if (e == cudaSuccess) e = optin<2, CHOL>();
+  if (e == cudaSuccess) e = optin<3, CHOL>();
+  if (e == cudaSuccess) e = optin<4, CHOL>();
+  if (e == cudaSuccess) e = optin<5, CHOL>();
+  if (e == cudaSuccess) e = optin<6, CHOL>();
+  if (e == cudaSuccess) e = optin<7, CHOL>();
+  if (e == cudaSuccess) e = optin<8, CHOL>();
+  return e;
+}
+
 long long count_tasks(bool chol, int n, int by, int bx) {
   const int nt = n / bx;
   long long total = 0;
@@ -1224,6 +1251,11 @@ long long count_tasks(bool chol, int n, int by, int bx) {
 }
 
 }  // namespace
+
+cudaError_t configure_device() {
+  const cudaError_t e = optin_all<false>();
+  return e != cudaSuccess ? e : optin_all<true>();
+}
 
 bool eligible(int n, int by, int bx) {
   if (bx < kMinTile || bx > kMaxTile || n % bx || by < 1 || n % by) return false;

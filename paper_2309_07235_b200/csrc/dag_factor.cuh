@@ -39,6 +39,10 @@ constexpr long long kMaxTasks = 8LL << 20;
 constexpr long long kWatchdogNs = 4000000000LL;
 constexpr int kTimeout = -2147483647 - 1;  // INT_MIN
 
+// Opts every persistent-kernel variant into its shared memory on the
+// current device (called per context: the attribute is per device).
+cudaError_t configure_device();
+
 // True when the persistent schedule covers (n, by, bx).
 bool eligible(int n, int by, int bx);
 

@@ -1,5 +1,6 @@
 // Instantiation helper for the AOT DMMA GEMM family.
 #pragma once
+#include "devattr.hpp"
 #include "gemm.hpp"
 
 namespace tt {
@@ -8,13 +9,9 @@ template <int BM, int BN, bool BT>
 cudaError_t launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                            const GemmArgs& args, long long grid, cudaStream_t stream) {
   using S = GemmShape<BM, BN, BT>;
-  static bool configured = false;  // per-variant attribute set once per process
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<BM, BN, BT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<unsigned long long> configured{0};  // per variant, one bit per device
+  const cudaError_t e = smem_optin(dgemm_kernel<BM, BN, BT>, S::SMEM, configured);
+  if (e != cudaSuccess) return e;
   if (grid <= 0) return cudaSuccess;
   dgemm_kernel<BM, BN, BT><<<static_cast<unsigned>(grid), S::THREADS, S::SMEM, stream>>>(ta, tb, tc,
                                                                                          args);

@@ -92,6 +92,25 @@ int fail(tt_ctx* ctx, int code, const char* fmt, ...) {
   return code;
 }
 
+// Makes the context's device current for the scope of a device-pointer entry
+// point and restores the caller's device afterwards (the caller's thread may
+// have another GPU current: the workspace allocation and the SM count of the
+// persistent schedule, and graph capture, must all happen on ctx->device).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+    if (prev == dev) prev = -1;  // nothing to restore
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 int cuda_fail(tt_ctx* ctx, cudaError_t e, const char* where) {
   if (e == cudaErrorMemoryAllocation)
     return fail(ctx, TT_ENOMEM, "%s: %s", where, cudaGetErrorString(e));
@@ -334,17 +353,20 @@ int enqueue_run(tt_ctx* ctx, const int* cfg, cudaEvent_t ev_start, cudaEvent_t e
   cudaGraphExec_t g = nullptr;
   long long nodes = 0;
   int rc;
+  // build (or fetch) the instantiation first: workspace allocation, capture
+  // and cudaGraphInstantiate stay outside the event pair even with 0 warm-ups
+  // (TT_EAGER=1 has no graph: the schedule is enqueued inside the pair)
+  auto build = [&] {
+    return ctx->kernel == TT_KERNEL_MM3
+               ? mm3_graph(ctx, setup_mm3_bufs(ctx), ctx->dims, cfg, &g, &nodes)
+               : factor_graph(ctx, ctx->kernel, ctx->work.p, ctx->dims[0], ctx->work.ld, cfg[0],
+                              cfg[1], &g, &nodes);
+  };
+  if (!eager_mode() && (rc = build()) != TT_OK) return rc;
   if (ctx->kernel != TT_KERNEL_MM3)  // fresh copy of the pristine input, untimed
     TT_CUDA(ctx, copy_d2d(ctx->work, ctx->pristine[0], ctx->stream), "restore copy");
   if (ev_start) TT_CUDA(ctx, cudaEventRecord(ev_start, ctx->stream), "cudaEventRecord");
-  if (ctx->kernel == TT_KERNEL_MM3) {
-    tt::Mm3Bufs b = setup_mm3_bufs(ctx);
-    rc = mm3_graph(ctx, b, ctx->dims, cfg, &g, &nodes);
-  } else {
-    rc = factor_graph(ctx, ctx->kernel, ctx->work.p, ctx->dims[0], ctx->work.ld, cfg[0], cfg[1],
-                      &g, &nodes);
-  }
-  if (rc) return rc;
+  if (eager_mode() && (rc = build()) != TT_OK) return rc;
   if (g) TT_CUDA(ctx, cudaGraphLaunch(g, ctx->stream), "cudaGraphLaunch");
   if (ev_end) TT_CUDA(ctx, cudaEventRecord(ev_end, ctx->stream), "cudaEventRecord");
   ctx->launches += static_cast<unsigned long long>(nodes);
@@ -532,6 +554,8 @@ int tt_ctx_create(int device, tt_ctx** out) {
                            : tt::launch_nn(bm, bn, m, m, m, dummy, 0, ctx->stream);
         if (r != cudaSuccess) return cleanup(TT_EDEVICE);
       }
+  // and every persistent-schedule variant (the attribute is per device)
+  if (tt::dag::configure_device() != cudaSuccess) return cleanup(TT_EDEVICE);
   *out = ctx;
   return TT_OK;
 }
@@ -879,6 +903,9 @@ int tt_dev_lu(tt_ctx* ctx, double* a, int n, int ld, int by, int bx, int* fail_i
   int rc = validate_factor(ctx, TT_KERNEL_LU, n, n, by, bx);
   if (rc) return rc;
   if (ld < n || (ld & 1)) return fail(ctx, TT_EINVAL, "leading dimension must be even and >= n");
+  if (!aligned16(a)) return fail(ctx, TT_EINVAL, "matrix base must be 16-byte aligned");
+  DeviceGuard dg(ctx->device);
+  TT_CUDA(ctx, dg.err, "cudaSetDevice");
   cudaGraphExec_t g = nullptr;
   long long nodes = 0;
   rc = factor_graph(ctx, TT_KERNEL_LU, a, n, ld, by, bx, &g, &nodes);
@@ -908,6 +935,9 @@ int tt_dev_cholesky(tt_ctx* ctx, double* a, int n, int ld, int by, int bx, int* 
   int rc = validate_factor(ctx, TT_KERNEL_CHOLESKY, n, n, by, bx);
   if (rc) return rc;
   if (ld < n || (ld & 1)) return fail(ctx, TT_EINVAL, "leading dimension must be even and >= n");
+  if (!aligned16(a)) return fail(ctx, TT_EINVAL, "matrix base must be 16-byte aligned");
+  DeviceGuard dg(ctx->device);
+  TT_CUDA(ctx, dg.err, "cudaSetDevice");
   cudaGraphExec_t g = nullptr;
   long long nodes = 0;
   rc = factor_graph(ctx, TT_KERNEL_CHOLESKY, a, n, ld, by, bx, &g, &nodes);
@@ -938,6 +968,15 @@ int tt_dev_mm3(tt_ctx* ctx, const double* a, int lda, const double* b, int ldb, 
   if (!ctx || !a || !b || !c || !d || !e || !f || !g || !cfg) return TT_EINVAL;
   int rc = validate_mm3(ctx, n, l, m, o, p, cfg, ncfg);
   if (rc) return rc;
+  for (const void* q : {static_cast<const void*>(a), static_cast<const void*>(b),
+                        static_cast<const void*>(c), static_cast<const void*>(d),
+                        static_cast<const void*>(e), static_cast<const void*>(f),
+                        static_cast<const void*>(g)})
+    if (!aligned16(q)) return fail(ctx, TT_EINVAL, "3mm: operand bases must be 16-byte aligned");
+  if ((lda | ldb | ldc | ldd | lde | ldf | ldg) & 1)
+    return fail(ctx, TT_EINVAL, "3mm: leading dimensions must be even");
+  DeviceGuard dg(ctx->device);
+  TT_CUDA(ctx, dg.err, "cudaSetDevice");
   tt::Mm3Bufs bufs{a, b, c, d, lda, ldb, ldc, ldd, e, f, g, lde, ldf, ldg};
   const int dims[5] = {n, l, m, o, p};
   cudaGraphExec_t gx = nullptr;
@@ -953,6 +992,8 @@ int tt_dev_mm3(tt_ctx* ctx, const double* a, int lda, const double* b, int ldb, 
 int tt_dev_fill_uniform(tt_ctx* ctx, double* a, int rows, int cols, int ld, long long row0,
                         uint64_t seed, int stream_id, void* stream) {
   if (!ctx || !a || rows < 0 || cols < 0 || ld < cols) return TT_EINVAL;
+  DeviceGuard dg(ctx->device);
+  TT_CUDA(ctx, dg.err, "cudaSetDevice");
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   tt::launch_fill_uniform(a, ld, rows, cols, row0, seed, stream_id, s);
   TT_CUDA(ctx, cudaGetLastError(), "fill_uniform");
@@ -1007,6 +1048,8 @@ int tt_dev_gemm(tt_ctx* ctx, const double* a, int lda, const double* b, int ldb,
   rc = require_tile(ctx, fx, N, "matmul_tiled");
   if (rc) return rc;
   if ((lda & 1) || (ldb & 1)) return fail(ctx, TT_EINVAL, "gemm: leading dims must be even");
+  DeviceGuard dg(ctx->device);
+  TT_CUDA(ctx, dg.err, "cudaSetDevice");
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   const tt::Operand A{a, M, std::max(K, 1), lda, 0, 0};
   const tt::Operand B = b_trans ? tt::Operand{b, N, std::max(K, 1), ldb, 0, 0}

@@ -1,0 +1,169 @@
+"""Oracle parity at the configurations the bench reports (BASELINE.json configs).
+
+Every bench workload is checked here against the CPU oracle (the C restatement of
+/root/reference/proj/core/src/kernels.cpp, bitwise equal to the unmodified
+reference core) on the same inputs, at the north_star tolerances:
+
+* LU / Cholesky: max-norm residual ||A - LU|| / ||A||, ||A - LL^T|| / ||A|| <= 1e-12,
+  and the factors themselves within 1e-10 (max relative) of the oracle's factors;
+* 3mm: max relative error of G <= 1e-10 against mm3_reference (kernels.cpp:115-120).
+
+The oracle's tiled outputs are config-independent bitwise, so one
+oracle run per (kernel, size) pins every GPU config; the fixtures below compute it
+once per session.  Inputs come from the device generator (bitwise gen_spd /
+gen_3mm_inputs, pinned in test_gpu_kernels.py) so the oracle does not spend
+38 s in gen_spd(4000).  Residuals use numpy BLAS as the checker.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2309_07235_b200 import GpuKernelRunner, KernelCase
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+LARGE3 = (800, 900, 1000, 1100, 1200)
+XL3 = (1600, 1800, 2000, 2200, 2400)
+
+
+def rel(x, ref):
+    return float(np.max(np.abs(x - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+def lu_residual(a, packed):
+    l = np.tril(packed, -1)
+    np.fill_diagonal(l, 1.0)
+    return float(np.max(np.abs(l @ np.triu(packed) - a)) / np.max(np.abs(a)))
+
+
+def chol_residual(a, w):
+    l = np.tril(w)
+    return float(np.max(np.abs(l @ l.T - a)) / np.max(np.abs(a)))
+
+
+class _Cache:
+    def __init__(self):
+        self.d = {}
+
+    def get(self, key, make):
+        if key not in self.d:
+            self.d[key] = make()
+        return self.d[key]
+
+
+@pytest.fixture(scope="module")
+def cache():
+    return _Cache()
+
+
+def factor_case(ctx, cache, kernel, n):
+    runner = GpuKernelRunner(KernelCase(kernel, n, seed=1), ctx)
+
+    def make():
+        (a,) = runner.inputs()
+        ref = a.copy()
+        # config-independent bitwise on the CPU: the cheapest knob setting
+        if kernel == "lu":
+            oracle.lu_factor_inplace(ref, n, n)
+        else:
+            oracle.cholesky_factor_inplace(ref, 50, 50)
+        return a, ref
+
+    a, ref = cache.get((kernel, n), make)
+    return runner, a, ref
+
+
+@pytest.mark.parametrize("n,cfg", [(2000, (200, 40)), (4000, (160, 50)), (4000, (250, 40)),
+                                   (4000, (500, 50))])
+def test_lu_bench_configs_vs_oracle(gpu_ctx, cache, n, cfg):
+    """LU LARGE at the bench's fixed block and LU XL at the bench / BO configs
+    (kernels.cpp:178-218)."""
+    runner, a, ref = factor_case(gpu_ctx, cache, "lu", n)
+    w = runner.run(cfg)
+    assert rel(w, ref) <= 1e-10, cfg
+    assert lu_residual(a, w) <= 1e-12, cfg
+    assert runner.residual() <= 1e-12, cfg  # the device residual agrees
+
+
+@pytest.mark.parametrize("cfg", [(250, 50), (80, 32), (200, 40), (500, 40), (160, 25)])
+def test_cholesky_xl_vs_oracle(gpu_ctx, cache, cfg):
+    """Cholesky XL (configs[2], kernels.cpp:264-308) at the round-1 BO best (250, 50),
+    the paper's A100 best (80, 32) and the persistent-schedule block widths."""
+    n = 4000
+    runner, a, ref = factor_case(gpu_ctx, cache, "cholesky", n)
+    w = runner.run(cfg)
+    il = np.tril_indices(n)
+    assert rel(w[il], ref[il]) <= 1e-10, cfg
+    iu = np.triu_indices(n, 1)
+    assert np.array_equal(w[iu], a[iu]), "upper triangle must be untouched"
+    assert chol_residual(a, w) <= 1e-12, cfg
+
+
+def test_cholesky_xl_never_reads_upper(gpu_ctx, cache):
+    """The reference reads only j <= i (kernels.cpp:273-306): garbage (NaN / huge)
+    in the strict upper triangle must neither change L nor be overwritten."""
+    n = 4000
+    _, a, ref = factor_case(gpu_ctx, cache, "cholesky", n)
+    bad = a.copy()
+    iu = np.triu_indices(n, 1)
+    rng = np.random.default_rng(7)
+    bad[iu] = np.where(rng.random(len(iu[0])) < 0.5, np.nan, 1e300)
+    for cfg in ((250, 50), (200, 40)):
+        r = GpuKernelRunner(KernelCase("cholesky", n), gpu_ctx, inputs=[bad])
+        w = r.run(cfg)
+        il = np.tril_indices(n)
+        assert rel(w[il], ref[il]) <= 1e-10, cfg
+        assert np.array_equal(w[iu], bad[iu], equal_nan=True), cfg
+
+
+def mm3_case(ctx, cache, dims):
+    runner = GpuKernelRunner(KernelCase("3mm", *dims, seed=1), ctx)
+
+    def make():
+        mats = runner.inputs()
+        return oracle.mm3_reference(*mats)
+
+    return runner, cache.get(("3mm", dims), make)
+
+
+@pytest.mark.parametrize("cfg", [(100, 125, 125, 120, 32, 60), (80, 200, 200, 240, 80, 240),
+                                 (25, 25, 25, 30, 25, 30)])
+def test_mm3_large_bench_configs_vs_oracle(gpu_ctx, cache, cfg):
+    """3mm LARGE (configs[0], kernels.cpp:122-131) at the bench's fixed tile config,
+    the survey's GPU-friendly example and the CPU's synthetic optimum."""
+    runner, gref = mm3_case(gpu_ctx, cache, LARGE3)
+    g = runner.run(cfg)
+    assert rel(g, gref) <= 1e-10, cfg
+
+
+@pytest.mark.parametrize("cfg", [(64, 125, 125, 300, 64, 240), (64, 250, 1000, 16, 200, 24),
+                                 (64, 4, 1000, 32, 32, 32), (1600, 2000, 2000, 2400, 1600, 2400)])
+def test_mm3_xl_vs_oracle(gpu_ctx, cache, cfg):
+    """3mm XL (configs[3], the BO run's case) at the grid-searched config, two
+    round-1 BO bests and the whole-matrix single-CTA extreme."""
+    runner, gref = mm3_case(gpu_ctx, cache, XL3)
+    g = runner.run(cfg)
+    assert rel(g, gref) <= 1e-10, cfg
+
+
+@pytest.mark.parametrize("kernel", ["lu", "cholesky"])
+def test_huge_pivots_divide_exactly(gpu_ctx, kernel):
+    """Pivots beyond 2^1022 (1/pivot subnormal): the reference divides exactly
+    (kernels.cpp:191, :293-295); the GPU's reciprocal seed must not flush to 0."""
+    a = oracle.gen_spd(64, 1) * 2.0 ** 1011  # diagonal ~ 2^1022.4 .. 2^1023
+    assert np.max(np.abs(np.diag(a))) > 2.0 ** 1022
+    for cfg in ((8, 8), (16, 32), (64, 64), (32, 16)):
+        ref = a.copy()
+        w = a.copy()
+        if kernel == "lu":
+            oracle.lu_factor_inplace(ref, *cfg)
+            from paper_2309_07235_b200 import lu_factor_inplace
+            lu_factor_inplace(w, *cfg, ctx=gpu_ctx)
+            assert rel(w, ref) <= 1e-10, cfg
+        else:
+            oracle.cholesky_factor_inplace(ref, *cfg)
+            from paper_2309_07235_b200 import cholesky_factor_inplace
+            cholesky_factor_inplace(w, *cfg, ctx=gpu_ctx)
+            il = np.tril_indices(64)
+            assert rel(w[il], ref[il]) <= 1e-10, cfg
+        assert np.all(np.isfinite(w[np.tril_indices(64)])), cfg
