@@ -149,11 +149,16 @@ int tt_dev_fill_uniform(tt_ctx* ctx, double* a, int rows, int cols, int ld, long
                         uint64_t seed, int stream_id, void* stream);
 
 /* Persistent tile-DAG schedule (dag_factor.cu), host-side introspection:
- * writes up to `cap` tasks as int quadruples {kind | j << 2, k, r0, r1}
- * (kind 0 DIAG, 1 TRSM_L, 2 TRSM_U, 3 GEMM) and returns the task count, or
- * -1 when (n, by, bx) runs on the launch-per-kernel graph schedule instead.
- * Needs no device. */
+ * writes up to `cap` tasks as int quadruples {kind | j << 2, k0 | q << 16,
+ * r0, r1} (kind 0 DIAG, 1 TRSM_L, 2 TRSM_U, 3 GEMM; a GEMM applies the
+ * updates of panel steps [k0, k0+q) to rows [r0, r1) of tile column j, every
+ * other task has q = 1) and returns the task count, or -1 when (n, by, bx)
+ * runs on the launch-per-kernel graph schedule instead.  Needs no device. */
 int tt_dag_tasks(int kernel, int n, int by, int bx, int* out, int cap);
+/* Chunk depth d of that schedule: bulk tiles receive their updates d steps
+ * at a time (K = d * bx), the last 1..d steps of each tile singly; -1 when
+ * the graph schedule runs. */
+int tt_dag_chunk_depth(int n, int by, int bx);
 /* Number of leading tasks of that list forming the urgent queue (the rest is
  * the bulk queue); -1 when the graph schedule runs instead. */
 int tt_dag_urgent(int kernel, int n, int by, int bx);

@@ -35,6 +35,8 @@ typedef struct {
   double elapsed_s;    /* since the clock started (virtual for synthetic runs) */
   double best_so_far_s;
   int worker;          /* evaluator (device slot) that measured it */
+  double ask_s;        /* host time spent asking for it (its share of a batch ask) */
+  double eval_s;       /* wall time of its evaluation */
 } tt_record;
 
 /* ---- search space (space.hpp:41-68) ---- */
@@ -63,12 +65,29 @@ int tt_tune_synthetic(int tuner, int kernel, const char* size, uint64_t seed, in
 /* Measured objective on the GPUs: one worker per entry of `devices`, inputs
  * generated on every device from `input_seed` before the clock starts, the
  * reference's spot check (mini size, config_at(space, size/2), residual <=
- * 1e-10) first when `spot_check`, then tt_measure with the protocol. */
+ * 1e-10) first when `spot_check`, then tt_measure with the protocol.  With
+ * several devices the surrogate is fitted once per batch of n_devices
+ * candidates, handed out as devices go idle.  A device failure
+ * (MeasurementError) retires that worker and its candidate is re-evaluated
+ * on another device; when every worker failed the call returns TT_EDEVICE
+ * with the partial trace in out / *n_out (harness.cpp:252-256 flushes the
+ * partial trace before rethrowing).  Test hook: TT_FAULT_INJECT="w:n" makes
+ * worker w fail at its n-th evaluation (0-based). */
 int tt_tune_measured(int tuner, int kernel, const char* size, uint64_t seed,
                      uint64_t input_seed, int max_evals, double max_seconds,
                      const int* devices, int n_devices, int warmups, int reps, int aggregate,
                      int spot_check, tt_record* out, int cap, int* n_out, double* total_s,
                      char* err, int errcap);
+
+/* Virtual-clock measured run (the T1 / T8 time-to-best harness): n_virtual
+ * evaluators emulated on ONE real device.  Every candidate is measured for
+ * real (tt_measure) and occupies its virtual evaluator for the wall time the
+ * evaluation took; the real host ask time is charged serially; results reach
+ * the tuner at their virtual finish time.  elapsed_s is virtual time. */
+int tt_tune_virtual(int tuner, int kernel, const char* size, uint64_t seed, uint64_t input_seed,
+                    int max_evals, double max_seconds, int device, int n_virtual, int warmups,
+                    int reps, int aggregate, int spot_check, tt_record* out, int cap, int* n_out,
+                    double* total_s, char* err, int errcap);
 
 #ifdef __cplusplus
 }

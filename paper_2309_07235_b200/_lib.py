@@ -26,7 +26,7 @@ EXPORTS = (
     "tt_setup_host", "tt_setup_seeded", "tt_run", "tt_measure", "tt_measure_samples",
     "tt_get_input", "tt_residual", "tt_dev_lu", "tt_dev_cholesky", "tt_dev_mm3",
     "tt_dev_gemm", "tt_dev_fill_uniform", "tt_launch_count", "tt_build_info", "tt_dag_tasks",
-    "tt_dag_trace", "tt_dag_urgent", "tt_lu_factor_batch", "tt_cholesky_factor_batch",
+    "tt_dag_trace", "tt_dag_urgent", "tt_dag_chunk_depth", "tt_lu_factor_batch", "tt_cholesky_factor_batch",
 )
 
 _lib = None
@@ -73,6 +73,7 @@ def load() -> ctypes.CDLL:
         "tt_dag_tasks": (c_int, [c_int, c_int, c_int, c_int, c_int_p, c_int]),
         "tt_dag_trace": (c_int, [vp, vp, c_int]),
         "tt_dag_urgent": (c_int, [c_int, c_int, c_int, c_int]),
+        "tt_dag_chunk_depth": (c_int, [c_int, c_int, c_int]),
         "tt_lu_factor_batch": (c_int, [vp, vp, c_int, c_int, c_int, c_int, c_int_p]),
         "tt_cholesky_factor_batch": (c_int, [vp, vp, c_int, c_int, c_int, c_int, c_int_p]),
     }
@@ -97,7 +98,8 @@ def int_array(values) -> ctypes.Array:
 
 def dag_tasks(kernel: str, n: int, by: int, bx: int) -> np.ndarray | None:
     """Task list of the persistent tile-DAG schedule as an (ntasks, 4) int array
-    {kind | j << 2, k, r0, r1}, or None when (n, by, bx) uses the graph schedule."""
+    {kind | j << 2, k0 | q << 16, r0, r1} (a GEMM applies panel steps [k0, k0+q)),
+    or None when (n, by, bx) uses the graph schedule."""
     lib = load()
     kid = KERNEL_IDS[kernel]
     cnt = lib.tt_dag_tasks(kid, n, by, bx, None, 0)
@@ -106,3 +108,9 @@ def dag_tasks(kernel: str, n: int, by: int, bx: int) -> np.ndarray | None:
     out = np.zeros((cnt, 4), dtype=np.int32)
     lib.tt_dag_tasks(kid, n, by, bx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), cnt)
     return out
+
+
+def dag_chunk_depth(n: int, by: int, bx: int) -> int | None:
+    """Chunk depth d of the persistent schedule for (n, by, bx), None on the graph schedule."""
+    d = load().tt_dag_chunk_depth(n, by, bx)
+    return None if d < 0 else int(d)

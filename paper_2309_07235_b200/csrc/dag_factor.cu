@@ -40,15 +40,31 @@ constexpr int kStrip = 8 * kMF;   // rows per warp strip
 // pair exactly twice — the 2-wavefront minimum for 256 bytes.
 constexpr int kNP = 68;
 constexpr int kNoLower = INT_MAX / 2;
-// Per-warp double-buffered A strips (16 rows x <= 66 columns, row stride
-// kAW == 4 mod 16: conflict-free A-fragment loads) staged by cp.async.cg.
+constexpr int kSmemB = kIB * kNP;                // one walker tile / the TRSM M tile
+// single-step GEMM tasks: per-warp double-buffered A strips (16 rows x <= 66
+// columns, row stride kAW == 4 mod 16: conflict-free A-fragment loads)
+// staged by cp.async.cg after the B tile
 constexpr int kAW = 68;
 constexpr int kABuf = kStrip * kAW;              // doubles per buffer
-constexpr int kSmemB = kIB * kNP;                // B / M tile
 constexpr int kSmemA = kWarps * 2 * kABuf;       // all warps' A buffers
 // walker-only: DIAG block inverses (1024) + the U12-solve block inverses (512)
 constexpr int kSmemW = 1536;
-constexpr int kSmemBytes = (kSmemB + kSmemA + 9 * 64 + 2 * 132 + 128 + kSmemW) * 8;
+// walker: tiles D, L(k+1,k), U(k,k+1), the reciprocals rk (128) and the inverses
+constexpr int kWalkerSmem = 3 * kSmemB + 128 + kSmemW;
+// Dynamic shared memory of every CTA (one CTA per SM): the walker's tiles, a
+// queue CTA's TRSM tile + block inverses, or a GEMM task's q stacked B tiles.
+constexpr int kSmemBytes = 224 * 1024;
+constexpr int kBudget = kSmemBytes / 8;  // doubles
+static_assert(kWalkerSmem <= kBudget, "walker tiles exceed shared memory");
+static_assert(kSmemB + kSmemA <= kBudget, "single-step GEMM staging exceeds shared memory");
+// Row strides (doubles) of the staged GEMM B tiles.  LU stages B[k][n] and
+// loads fragments with 8-byte loads (lanes t and t+1 two rows apart): a stride
+// == 4 (mod 8) puts them on opposite bank halves, the 2-wavefront minimum.
+// Cholesky stages B^T[n][k] and loads both k-halves of a permuted fragment
+// with one 16-byte load: == 8 (mod 16) keeps each 8-lane phase conflict-free.
+__host__ __device__ constexpr int bstride(int tp, bool chol) {
+  return chol ? (tp % 16 == 8 ? tp : tp + 8) : tp + 4;
+}
 constexpr int kSolveSlot = 64;  // per step: diagonal reciprocals written by DIAG
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -77,6 +93,7 @@ struct Params {
   double* solve;  // per step: 64 reciprocals of the factored diagonal (DIAG -> TRSM)
   int nurgent;    // tasks[0, nurgent): urgent queue; [nurgent, ntasks): bulk queue
   int nuw;        // CTAs 1..nuw serve the urgent queue
+  int d;          // chunk depth (dag_factor.cuh)
   int eager_sig;  // publish GEMM strips right after their stores: 0 no, 1 all, 2 urgent, 3 bulk
   int pf_mask;    // bit 0: urgent CTAs, bit 1: bulk CTAs fetch the next task before
                   // the current one's dependency wait (else when warp 0 finishes it)
@@ -130,43 +147,56 @@ __device__ bool wait_ge(const Params& p, const int* addr, int need) {
   return true;
 }
 
+// Counter targets (finished rows) under the chunked stage numbering
+// (dag_factor.cuh): a tile with m updates has finished the stages covering
+// the steps < s, resp. is final.
+__device__ __forceinline__ int need_before(const Params& p, int m, int s) {
+  return stages_before(m, s, p.d) * p.T;
+}
+__device__ __forceinline__ int need_final(const Params& p, int m) {
+  return stages_total(m, p.d) * p.T;
+}
+
 // Task-level dependencies: what the whole CTA reads (the diagonal tile, the
 // B operand).  Row-strip dependencies (the strip's own output tiles and its
 // L rows) are waited for per strip by the warp that processes it, so a
 // task's first strips start as soon as their rows are ready (dataflow along
 // the rows: DIAG(k) -> first TRSM_L strips -> first GEMM strips -> DIAG(k+1)).
-template <bool CHOL>
-__device__ __forceinline__ int dep_count(int kind) {
-  return kind == kTrsmU ? 2 : 1;
-}
+// A GEMM over steps [k0, kl] waits only for the operands of step kl: U(kl, j)
+// final implies tile (kl, j) received the step kl-1 update, whose operand
+// U(kl-1, j) was therefore final (and so on down to k0); the same holds for
+// L(i, kl) / L(j, kl).  Acquire/release is transitive, so the chain makes the
+// earlier tiles visible as well.
+__device__ __forceinline__ int dep_count(int kind) { return kind == kTrsmU ? 2 : 1; }
 
 template <bool CHOL>
 __device__ __forceinline__ void dep_at(const Params& p, int kind, int j, int k, int d, int* idx,
                                        int* need) {
-  const int T = p.T, nt = p.nt, kT = k * T;
+  const int nt = p.nt;
   switch (kind) {
-    case kDiag:  // stage k-1 of tile (k,k)
-      *idx = k * nt + k;
-      *need = kT;
-      return;
     case kTrsmL:  // DIAG(k)
       *idx = k * nt + k;
-      *need = kT + T;
+      *need = need_final(p, k);
       return;
-    case kTrsmU:  // stage k-1 of tile (k,j), DIAG(k)
+    case kTrsmU:  // every update of tile (k,j), DIAG(k)
       *idx = d == 0 ? k * nt + j : k * nt + k;
-      *need = d == 0 ? kT : kT + T;
+      *need = d == 0 ? need_before(p, k, k) : need_final(p, k);
       return;
-    default:  // kGemm: B operand U(k, j) / L(j, k) final
+    default:  // kGemm over steps [k0, k]: B operand U(k, j) / L(j, k) final
       *idx = CHOL ? j * nt + k : k * nt + j;
-      *need = kT + T;
+      *need = need_final(p, k);
   }
 }
 
+// Task word: {kind | j << 2, k0 | q << 16, r0, r1}.
+__device__ __forceinline__ int task_k0(int4 tk) { return tk.y & 0xFFFF; }
+__device__ __forceinline__ int task_q(int4 tk) { return max(1, tk.y >> 16); }
+
 template <bool CHOL>
 __device__ bool wait_deps(const Params& p, int4 tk) {
-  const int kind = tk.x & 3, j = tk.x >> 2, k = tk.y;
-  const int nd = dep_count<CHOL>(kind);
+  const int kind = tk.x & 3, j = tk.x >> 2;
+  const int k = kind == kGemm ? task_k0(tk) + task_q(tk) - 1 : task_k0(tk);
+  const int nd = dep_count(kind);
   bool ok = true;
   const int d = threadIdx.x & 31;
   if (d < nd) {
@@ -177,20 +207,21 @@ __device__ bool wait_deps(const Params& p, int4 tk) {
   return __all_sync(0xffffffffu, ok);
 }
 
-// Row-strip dependencies of rows [rs, re) writing tile column `col` at step
-// k: stage k-1 of the output tiles, and (GEMM) the L tiles (i, k) final.
-// Lane d of the calling warp takes dependency d.  With `block` false this is
-// a single poll (true only if everything is already satisfied).
-__device__ __forceinline__ bool strip_deps(const Params& p, int rs, int re, int col, int k,
-                                           bool gemm, bool block) {
-  const int T = p.T, nt = p.nt, kT = k * T;
+// Row-strip dependencies of rows [rs, re) writing tile column `col` with the
+// stage that starts at step s: the output tiles' earlier stages, and (kl >= 0,
+// GEMM) the L tiles (i, kl) final.  Lane d of the calling warp takes
+// dependency d.  With `block` false this is a single poll (true only if
+// everything is already satisfied).
+__device__ __forceinline__ bool strip_deps(const Params& p, int rs, int re, int col, int s,
+                                           int kl, bool block) {
+  const int T = p.T, nt = p.nt;
   const int ti0 = rs / T, nti = (re - 1) / T - ti0 + 1;
   const int d = threadIdx.x & 31;
   bool ok = true;
-  if (d < (gemm ? 2 * nti : nti)) {
+  if (d < (kl >= 0 ? 2 * nti : nti)) {
     const int i = ti0 + (d < nti ? d : d - nti);
-    const int* c = &p.cnt[i * nt + (d < nti ? col : k)];
-    const int need = d < nti ? kT : kT + T;
+    const int* c = &p.cnt[i * nt + (d < nti ? col : kl)];
+    const int need = d < nti ? need_before(p, min(i, col), s) : need_final(p, kl);
     if (block) {
       ok = wait_ge(p, c, need);
     } else {
@@ -215,13 +246,14 @@ __device__ __forceinline__ void warp_signal(const Params& p, int ra, int rb, int
 
 
 // ---------------------------------------------------------------- GEMM
-// One warp's share of a GEMM task: C[r, c] -= sum_k A[r, k] * B[k, c] over
-// the 16-row strips ra = r0 + 16*warp, +128, ... of rows [r0, r1).  B (Kp x
-// Tp, zero-padded) is in shared memory.  Software pipeline per strip: the
-// next strip's A (cp.async.cg into the warp's other buffer, L2 only) and C
-// (registers) are in flight while this strip's DMMAs run; the strip is
-// published (fence + red.release) right after its stores.  Stores only
-// where row + lower_off >= col (Cholesky diagonal tiles).
+// ---- single-step tasks (q = 1, K = T): the near-diagonal band.
+// One warp's share: C[r, c] -= sum_k A[r, k] * B[k, c] over the 16-row strips
+// ra = r0 + 16*warp, +128, ... of rows [r0, r1).  B (Tp x Tp, zero-padded) is
+// in shared memory.  Software pipeline per strip: the next strip's A
+// (cp.async.cg into the warp's other buffer, L2 only) and C (registers) are
+// in flight while this strip's DMMAs run — with one step per strip the strip
+// round trip, not the DMMA work, is what a strip costs.  Stores only where
+// row + lower_off >= col (Cholesky diagonal tiles).
 // Operands of a strip task: rows r of [r0, r1) (global rows: tile counters)
 // read A from A0 + (r - r0)*lda (T columns) and update C at C0 + (r - r0)*ldc
 // (T columns of tile column cj); beta = 0 starts from zero instead of C.
@@ -295,7 +327,7 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
 
   double acc[kMF][NF][2];
   int prev_ra = -1, prev_nr = 0;
-  if (!strip_deps(p, ra, min(ra + kStrip, r1), j, k, op.gemm, true)) return;
+  if (!strip_deps(p, ra, min(ra + kStrip, r1), j, k, op.gemm ? k : -1, true)) return;
   if (first_done && lane == 0) first_done[2] = globaltimer();  // first strip's inputs final
   issue_a(ra, abuf);
   load_c(ra, acc);
@@ -305,7 +337,7 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
     const bool more = rn < r1;
     double cn[kMF][NF][2];
     // prefetch the next strip now if its rows are already final, else after this one
-    const bool pref = more && strip_deps(p, rn, min(rn + kStrip, r1), j, k, op.gemm, false);
+    const bool pref = more && strip_deps(p, rn, min(rn + kStrip, r1), j, k, op.gemm ? k : -1, false);
     if (pref) {
       issue_a(rn, abuf + (cur ^ 1) * kABuf);
       load_c(rn, cn);
@@ -371,7 +403,7 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
     }
     if (!more) break;
     if (!pref) {
-      if (!strip_deps(p, rn, min(rn + kStrip, r1), j, k, op.gemm, true)) return;  // aborted
+      if (!strip_deps(p, rn, min(rn + kStrip, r1), j, k, op.gemm ? k : -1, true)) return;  // aborted
       issue_a(rn, abuf + (cur ^ 1) * kABuf);
       load_c(rn, cn);
     }
@@ -384,6 +416,207 @@ __device__ __forceinline__ void gemm_strips(const Params& p, int r0, int r1, int
       }
     ra = rn;
     cur ^= 1;
+  }
+  if (prev_ra >= 0) warp_signal(p, prev_ra, prev_ra + prev_nr, j);
+}
+
+
+// ---- chunked tasks (q > 1):
+// C(rows, j) -= sum_{k in [k0, k0+q)} L(rows, k) * B_k,  B_k = U(k, j) (LU) or
+// L(j, k)^T (Cholesky), K = q*T.
+//
+// The q B tiles are staged once per task into shared memory (16-byte
+// cp.async of matrix rows, zero-filled padding).  Each warp takes 16-row
+// strips; a strip keeps -C in registers over all q steps and reads the L
+// rows straight from L2 into DMMA A fragments with 16-byte loads, the next
+// step's fragments in flight while the current step's DMMAs run.  The k index
+// inside every 8-wide block is permuted so a lane's two A values are
+// adjacent in memory: lane (g, t) supplies k = 8s + 2t + h for half h of the
+// k-block pair — the B fragments use the same permutation, so each DMMA still
+// forms a 4-term slice of the same dot product.  Accumulating into -C and
+// negating once per strip keeps every DMMA in its natural D = A*B + C form;
+// the values are exactly those of C + (-A)*B.
+__device__ __forceinline__ double negd(double x) {  // sign flip on the integer pipe
+  return __longlong_as_double(__double_as_longlong(x) ^ static_cast<long long>(0x8000000000000000ULL));
+}
+
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+// Stages B_k for k in [k0, k0+q) as q zero-padded Tp x Tp tiles of matrix
+// rows: LU  Bs[kk][x][y] = A[(k0+kk)T + x][jT + y]  (x = k index, y = n),
+//       Cholesky Bs[kk][y][x] = A[jT + y][(k0+kk)T + x]  (y = n, x = k).
+template <int NF, bool CHOL>
+__device__ __forceinline__ void stage_b(const Params& p, double* Bs, int j, int k0, int q) {
+  constexpr int Tp = NF * 8, NPB = bstride(Tp, CHOL), HP = Tp / 2;
+  const int T = p.T;
+  const long long ld = p.ld;
+  const int total = q * Tp * HP;  // element pairs
+  for (int e = threadIdx.x; e < total; e += kThreads) {
+    const int kk = e / (Tp * HP), rem = e - kk * (Tp * HP), x = rem / HP, y = 2 * (rem - x * HP);
+    const int k = k0 + kk;
+    const long long row = CHOL ? static_cast<long long>(j) * T + x : static_cast<long long>(k) * T + x;
+    const long long col = CHOL ? static_cast<long long>(k) * T + y : static_cast<long long>(j) * T + y;
+    const double* src = p.a + row * ld + col;
+    double* dst = Bs + kk * Tp * NPB + x * NPB + y;
+    if (!(T & 1)) {
+      const bool valid = x < T && y < T;
+      cp_async16_zfill(dst, valid ? src : p.a, valid);
+    } else {  // odd T: rows are not 16-byte aligned
+      dst[0] = (x < T && y < T) ? __ldcg(src) : 0.0;
+      dst[1] = (x < T && y + 1 < T) ? __ldcg(src + 1) : 0.0;
+    }
+  }
+  if (!(T & 1)) {
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
+}
+
+template <int NF, bool CHOL>
+__device__ void gemm_task(const Params& p, int j, int k0, int q, int r0, int r1,
+                          const double* __restrict__ Bs, bool eager,
+                          unsigned long long* first_done) {
+  constexpr int Tp = NF * 8, NPB = bstride(Tp, CHOL);
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
+  const int T = p.T;
+  const long long ld = p.ld;
+  const int kl = k0 + q - 1, jT = j * T;
+  const bool even = !(T & 1);  // element pairs of the L rows / C rows are 16-byte aligned
+
+  // A fragments of step k for the strip at rows ra: a[mf][s].x / .y = L(r, 8s+2t) / (8s+2t+1)
+  auto load_a = [&](double2 (&a)[kMF][NF], int ra, int nr, int k) {
+#pragma unroll
+    for (int mf = 0; mf < kMF; ++mf) {
+      const int r = mf * 8 + g;
+      const double* row = p.a + static_cast<long long>(ra + (r < nr ? r : 0)) * ld +
+                          static_cast<long long>(k) * T;
+#pragma unroll
+      for (int s = 0; s < NF; ++s) {
+        const int c = 8 * s + 2 * t;
+        double2 v = make_double2(0.0, 0.0);
+        if (r < nr) {
+          if (even) {
+            if (c < T) v = __ldcg(reinterpret_cast<const double2*>(row + c));
+          } else {
+            if (c < T) v.x = __ldcg(row + c);
+            if (c + 1 < T) v.y = __ldcg(row + c + 1);
+          }
+        }
+        a[mf][s] = v;
+      }
+    }
+  };
+  const bool cvec = even;  // C rows: same alignment argument (ld even, jT even)
+  int prev_ra = -1, prev_nr = 0;
+  for (int ra = r0 + warp * kStrip; ra < r1; ra += kWarps * kStrip) {
+    const int nr = min(kStrip, r1 - ra);
+    if (!strip_deps(p, ra, ra + nr, j, k0, kl, true)) return;  // aborted
+    if (first_done && lane == 0) first_done[2] = globaltimer();
+    double acc[kMF][NF][2];  // -C
+#pragma unroll
+    for (int mf = 0; mf < kMF; ++mf) {
+      const int r = mf * 8 + g;
+      const double* crow = p.a + static_cast<long long>(ra + (r < nr ? r : 0)) * ld + jT;
+#pragma unroll
+      for (int nf = 0; nf < NF; ++nf) {
+        const int c = nf * 8 + 2 * t;
+        double2 v = make_double2(0.0, 0.0);
+        if (r < nr) {
+          if (cvec) {
+            if (c < T) v = __ldcg(reinterpret_cast<const double2*>(crow + c));
+          } else {
+            if (c < T) v.x = __ldcg(crow + c);
+            if (c + 1 < T) v.y = __ldcg(crow + c + 1);
+          }
+        }
+        acc[mf][nf][0] = negd(v.x);
+        acc[mf][nf][1] = negd(v.y);
+      }
+    }
+    double2 a[kMF][NF];
+    load_a(a, ra, nr, k0);
+    for (int kk = 0; kk < q; ++kk) {
+      double2 an[kMF][NF];
+      if (kk + 1 < q) load_a(an, ra, nr, k0 + kk + 1);
+      if (first_done && lane == 0 && kk == 0) first_done[1] = globaltimer();
+      const double* B = Bs + kk * Tp * NPB;
+#pragma unroll
+      for (int s = 0; s < NF; ++s) {
+        if (8 * s < T) {
+          if (CHOL) {  // Bs[n][k]: both k-halves of lane t with one 16-byte load
+            double2 bv[NF];
+#pragma unroll
+            for (int nf = 0; nf < NF; ++nf)
+              bv[nf] = *reinterpret_cast<const double2*>(B + (8 * nf + g) * NPB + 8 * s + 2 * t);
+#pragma unroll
+            for (int mf = 0; mf < kMF; ++mf)
+#pragma unroll
+              for (int nf = 0; nf < NF; ++nf) {
+                dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a[mf][s].x, bv[nf].x);
+                dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a[mf][s].y, bv[nf].y);
+              }
+          } else {  // Bs[k][n]
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              double bv[NF];
+#pragma unroll
+              for (int nf = 0; nf < NF; ++nf) bv[nf] = B[(8 * s + 2 * t + h) * NPB + 8 * nf + g];
+#pragma unroll
+              for (int mf = 0; mf < kMF; ++mf)
+#pragma unroll
+                for (int nf = 0; nf < NF; ++nf)
+                  dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], h ? a[mf][s].y : a[mf][s].x, bv[nf]);
+            }
+          }
+        }
+      }
+      // publish the previous strip once this one's first DMMAs are issued:
+      // its stores went out a whole strip ago, so the release does not stall
+      if (kk == 0 && prev_ra >= 0) {
+        warp_signal(p, prev_ra, prev_ra + prev_nr, j);
+        prev_ra = -1;
+      }
+      if (kk + 1 < q) {
+#pragma unroll
+        for (int mf = 0; mf < kMF; ++mf)
+#pragma unroll
+          for (int s = 0; s < NF; ++s) a[mf][s] = an[mf][s];
+      }
+    }
+    const int lower_off = CHOL ? ra - jT : kNoLower;  // Cholesky: store only row >= col
+#pragma unroll
+    for (int mf = 0; mf < kMF; ++mf) {
+      const int r = mf * 8 + g;
+      if (r < nr) {
+        double* crow = p.a + static_cast<long long>(ra + r) * ld + jT;
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf) {
+          const int c = nf * 8 + 2 * t;
+          const double v0 = negd(acc[mf][nf][0]), v1 = negd(acc[mf][nf][1]);
+          const bool ok0 = c < T && r + lower_off >= c, ok1 = c + 1 < T && r + lower_off >= c + 1;
+          if (cvec && ok0 && ok1) {
+            *reinterpret_cast<double2*>(crow + c) = make_double2(v0, v1);
+          } else {
+            if (ok0) crow[c] = v0;
+            if (ok1) crow[c + 1] = v1;
+          }
+        }
+      }
+    }
+    if (first_done && lane == 0) {
+      first_done[0] = globaltimer();
+      first_done = nullptr;
+    }
+    if (eager) {
+      warp_signal(p, ra, ra + nr, j);
+    } else {
+      prev_ra = ra;
+      prev_nr = nr;
+    }
   }
   if (prev_ra >= 0) warp_signal(p, prev_ra, prev_ra + prev_nr, j);
 }
@@ -416,7 +649,6 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(r, e, r);
 }
 
-constexpr int kPB = 132;  // doubles per parity of the DIAG publication buffer
 
 
 // Blocked factorisation of the diagonal tile (T <= 64, NB = ceil(T/8) blocks)
@@ -797,7 +1029,7 @@ __device__ void walker(const Params& p, double* dsm) {
   double* D = dsm;                          // tile (k,k)
   double* Lt = dsm + kSmemB;                // tile (k+1,k): A21 -> L21
   double* Ut = Lt + kSmemB;                 // tile (k,k+1): A12 -> U12 (LU)
-  double* rk = dsm + kSmemB + kSmemA + 9 * 64 + 2 * kPB;  // 128
+  double* rk = Ut + kSmemB;                 // 128
   double* inv = rk + 128;                   // 1024: DIAG block inverses
   double* invX = inv + 1024;                // 512: inverses for the second solve
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -817,8 +1049,9 @@ __device__ void walker(const Params& p, double* dsm) {
     const int kT = k * T;
     double* dk = p.a + static_cast<long long>(kT) * ld + kT;
     stamp(k, 0);
-    // stages 0..k-2 of tile (k,k) come from the queue's GEMM tasks
-    if (k >= 2 && !wait1(&p.cnt[k * nt + k], (k - 1) * T)) return;
+    // the updates of steps < k-1 of tile (k,k) come from the queue's GEMM
+    // tasks (step k-1 is always a single step: the walker applies it)
+    if (k >= 2 && !wait1(&p.cnt[k * nt + k], need_before(p, k, k - 1))) return;
     stamp(k, 1);
     tile_load<CHOL>(D, dk, ld, T);
     __syncthreads();
@@ -871,8 +1104,8 @@ __device__ void walker(const Params& p, double* dsm) {
     if (!s_ok) return;
     if (k + 1 >= nt) break;
     // ---- first tiles of the panel: L(k+1,k) = A(k+1,k) U11^-1, U(k,k+1) = L11^-1 A(k,k+1)
-    if (!wait1(&p.cnt[(k + 1) * nt + k], kT)) return;
-    if (!CHOL && !wait1(&p.cnt[k * nt + k + 1], kT)) return;
+    if (!wait1(&p.cnt[(k + 1) * nt + k], need_before(p, k, k))) return;
+    if (!CHOL && !wait1(&p.cnt[k * nt + k + 1], need_before(p, k, k))) return;
     stamp(k, 4);
     {
       const double* al = p.a + static_cast<long long>(kT + T) * ld + kT;
@@ -977,8 +1210,8 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
   constexpr int Tp = NF * 8;
   extern __shared__ __align__(16) double dsm[];
   double* sm = dsm;                      // B (GEMM) / M (TRSM): Tp x kNP
-  double* abuf = dsm + kSmemB;           // per-warp A strips
-  double* minv = abuf + kSmemA;          // 8 x (8x8) block inverses + 64 diagonal reciprocals
+  double* minv = dsm + kSmemB;           // TRSM: 8 x (8x8) block inverses + 64 diagonal reciprocals
+  double* abuf = dsm + kSmemB;           // single-step GEMM: per-warp A strips
   __shared__ int4 s_task[2];
   __shared__ int s_id[2];
   __shared__ int s_go;
@@ -1032,7 +1265,7 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
     }
     __syncthreads();
     if (!s_go) break;
-    const int kind = tk.x & 3, j = tk.x >> 2, k = tk.y, r0 = tk.z, r1 = tk.w;
+    const int kind = tk.x & 3, j = tk.x >> 2, k = task_k0(tk), r0 = tk.z, r1 = tk.w;
     const int kT = k * T;
     double* dk = p.a + static_cast<long long>(kT) * ld + kT;  // diagonal tile (k,k)
 
@@ -1040,7 +1273,16 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
     stamp(1);
     stamp(2);
     stamp(3);
-    if (kind == kGemm) {
+    if (kind == kGemm && task_q(tk) > 1) {  // chunked: q steps, K = q*T
+      const int q = task_q(tk);
+      stage_b<NF, CHOL>(p, sm, j, k, q);
+      __syncthreads();
+      stamp(0);
+      // p.eager_sig: 0 none, 1 all GEMM tasks, 2 urgent-queue CTAs only, 3 bulk only
+      const bool eager =
+          p.eager_sig == 1 || (p.eager_sig == 2 && urgent_q) || (p.eager_sig == 3 && !urgent_q);
+      gemm_task<NF, CHOL>(p, j, k, q, r0, r1, sm, eager, (p.trace && warp == 0) ? &s_ph[1] : nullptr);
+    } else if (kind == kGemm) {  // single step
       // B = U(k, j) (LU) or L(j, k)^T (Cholesky), zero-padded to Tp x Tp
       const double* bsrc = CHOL ? p.a + static_cast<long long>(j * T) * ld + kT
                                 : p.a + static_cast<long long>(kT) * ld + j * T;
@@ -1148,7 +1390,7 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
       if (lsolve) {
         for (int ra = r0 + warp * kStrip; ra < r1; ra += kWarps * kStrip) {
           const int nr = min(kStrip, r1 - ra);
-          if (!strip_deps(p, ra, ra + nr, k, k, false, true)) break;
+          if (!strip_deps(p, ra, ra + nr, k, k, -1, true)) break;
           warp_trsm<NF>(p.a + static_cast<long long>(ra) * ld + kT, ld, 1, nr, T, sm, minv);
           warp_signal(p, ra, ra + nr, k);
         }
@@ -1245,7 +1487,8 @@ long long count_tasks(bool chol, int n, int by, int bx) {
     const int pe = (k + 1) * bx;
     const long long regions = (n - 1) / by - pe / by + 1;
     const long long cols = nt - k - 1;
-    total += regions + (chol ? 0 : cols) + regions * cols + 4;  // + carved pieces
+    // + carved pieces; chunked and single GEMMs may each split a region in two runs
+    total += regions + (chol ? 0 : cols) + 4 * regions * cols + 4;
   }
   return total;
 }
@@ -1315,56 +1558,100 @@ GemmMerge gemm_merge() {
   return g;
 }
 
-// Two queues, each in step order.  The urgent queue (served by a few
-// dedicated CTAs) holds what the walker needs next — per step k: the L21
-// rows of tile row k+2, U(k,k+2), and the GEMM rows of tiles (k+2,k+1),
-// (k+1,k+2), (k+2,k+2) — carved out of their row regions at the row
-// (k+3)*bx, so urgent tasks stay one or two tiles small; the bulk queue
-// holds the rest.  Deadlock-free: every task waits only on earlier steps,
-// walker steps <= its own, same-step tasks earlier in its own queue, or
-// (bulk only) same-step urgent tasks — urgent tasks never wait on same-step
-// bulk tasks (their rows lie above the carve row, as do the L21 rows they
-// read); the walker's step k+1 waits only on step-k tasks.  So the urgent
-// work of step k is never stuck behind the bulk of step k-1.
-// Returns urgent ++ bulk; *n_urgent = urgent count.
+// Chunk depth: steps per bulk GEMM task, K = d*T ~ 200 (TT_DAG_CHUNK=d
+// overrides; 1 = step-by-step updates), capped by the shared memory the q
+// stacked B tiles take.
+int chunk_depth(int bx) {
+  const int tp = (bx + 7) / 8 * 8;
+  const int cap = std::max(1, kBudget / (tp * std::max(bstride(tp, true), bstride(tp, false))));
+  const char* v = std::getenv("TT_DAG_CHUNK");  // read per workspace (tests vary it)
+  const int forced = v ? std::atoi(v) : 0;
+  const int d = forced >= 1 ? forced : (200 + bx / 2) / bx;
+  return std::max(1, std::min({d, cap, 0xFFFF / 2}));
+}
+
+// Two queues, each in "ready step" order.  A task's ready step is the last
+// panel step whose output it reads (TRSM_L/U(k): k; a GEMM over steps
+// [k0, k0+q): k0+q-1); per ready step r the queues hold TRSM_L(r), TRSM_U(r, j),
+// then the single-step GEMMs of step r, then (when r+1 closes a chunk) the
+// chunked GEMMs of steps [r+1-d, r+1).  The urgent queue (served by a few
+// dedicated CTAs) holds what the walker needs next — the L21 rows of tile
+// rows <= r+band and the U / GEMM pieces of tile columns <= r+band above the
+// carve row (r+1+band)*bx; the bulk queue holds the rest.  Deadlock-free:
+// every task waits only on tasks of earlier ready steps, walker steps <= its
+// own, same-step tasks earlier in its own queue (TRSM before GEMM), or (bulk
+// only) same-step urgent tasks — an urgent task never reads a same-step bulk
+// task's output (its rows and columns lie inside the band); walker step r+1
+// waits only on tasks of ready steps <= r.  Row regions are `by` rows (the
+// reference's trailing row tile, kernels.cpp:205-216) aligned to multiples
+// of by and clipped to the trailing rows; a GEMM region is further split at
+// the tiles where the (chunk / single step) stage structure changes
+// (dag_factor.cuh).  Returns urgent ++ bulk; *n_urgent = urgent count.
 std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
   const int T = bx, nt = n / bx;
+  const int d = chunk_depth(bx);
   const int band = urgent_band();
   const GemmMerge gm = gemm_merge();
   std::vector<int4> urg, bulk;
   bulk.reserve(static_cast<size_t>(count_tasks(chol, n, by, bx)));
-  for (int k = 0; k + 1 < nt; ++k) {
-    const int pe = (k + 1) * T;
-    const int carve = std::min(n, (k + 1 + band) * T);  // rows above: tile rows <= k+band
-    auto task = [&](int kind, int r0, int r1, int j) {
+  // is [k0, k0+q) one stage of tile (i, j)?
+  auto is_stage = [&](int i, int jj, int k0, int q) {
+    const int m = std::min(i, jj), nc = nchunks(m, d);
+    if (q == d && k0 % d == 0 && k0 + d <= nc * d) return true;  // a full chunk
+    return q == 1 && k0 >= nc * d && k0 < m;                      // a single step
+  };
+  for (int r = 0; r + 1 < nt; ++r) {
+    const int pe = (r + 1) * T;
+    const int carve = std::min(n, (r + 1 + band) * T);  // rows above: tile rows <= r+band
+    auto task = [&](int kind, int r0, int r1, int j, int k0, int q) {
       if (r0 >= r1) return;
-      const bool near = kind == kTrsmU ? j <= k + band : (kind == kTrsmL || j <= k + band);
+      const int y = k0 | (q << 16);
+      const bool near = kind == kTrsmU ? j <= r + band : (kind == kTrsmL || j <= r + band);
       if (near && r0 < carve) {  // split at the carve row
-        urg.push_back(make_int4(kind | (j << 2), k, r0, kind == kTrsmU ? r1 : std::min(r1, carve)));
-        if (kind != kTrsmU && r1 > carve) bulk.push_back(make_int4(kind | (j << 2), k, carve, r1));
+        urg.push_back(make_int4(kind | (j << 2), y, r0, kind == kTrsmU ? r1 : std::min(r1, carve)));
+        if (kind != kTrsmU && r1 > carve) bulk.push_back(make_int4(kind | (j << 2), y, carve, r1));
       } else {
-        bulk.push_back(make_int4(kind | (j << 2), k, r0, r1));
+        bulk.push_back(make_int4(kind | (j << 2), y, r0, r1));
       }
     };
     std::vector<std::pair<int, int>> reg;  // row regions: multiples of by, clipped
-    for (int r = (pe / by) * by; r < n; r += by) reg.emplace_back(std::max(r, pe), std::min(n, r + by));
-    for (const auto& rg : reg) task(kTrsmL, std::max(rg.first, pe + T), rg.second, 0);  // row k+1: walker
+    for (int x = (pe / by) * by; x < n; x += by) reg.emplace_back(std::max(x, pe), std::min(n, x + by));
+    for (const auto& rg : reg) task(kTrsmL, std::max(rg.first, pe + T), rg.second, 0, r, 1);  // row r+1: walker
     if (!chol)
-      for (int j = k + 2; j < nt; ++j) task(kTrsmU, 0, 1, j);
-    // row regions outer: a region's GEMMs need only that region's L21 rows
-    // (plus the U12 tiles), so the first GEMMs taken are the first ready.
-    // Steps with many GEMM tasks group `merge` consecutive regions per task
-    // (more strips per warp: the per-task latency is amortised).
-    const int ncols = nt - k - 1, nreg = static_cast<int>(reg.size());
+      for (int j = r + 2; j < nt; ++j) task(kTrsmU, 0, 1, j, r, 1);
+    // GEMM intervals ready at step r: the single step r, then the chunk
+    // [r+1-d, r+1) when r+1 closes one
+    std::vector<std::pair<int, int>> ivals{{r, 1}};
+    if (d > 1 && (r + 1) % d == 0) ivals.emplace_back(r + 1 - d, d);
+    const int ncols = nt - r - 1, nreg = static_cast<int>(reg.size());
     const bool merge = gm.rows > 0 && static_cast<long long>(nreg) * ncols >= gm.thresh;
-    for (int g0 = 0, g1; g0 < nreg; g0 = g1) {
-      g1 = g0 + 1;  // regions [g0, g1) form one task: at least gm.rows rows when merging
-      while (merge && g1 < nreg && reg[g1 - 1].second - reg[g0].first < gm.rows) ++g1;
-      const int lo = reg[g0].first, hi = reg[g1 - 1].second;
-      for (int j = k + 1; j < nt; ++j) {
-        int r0 = std::max(lo, chol ? j * T : pe);  // Cholesky: lower triangle only
-        if (j == k + 1) r0 = std::max(r0, pe + T);  // tile (k+1,k+1): the walker
-        task(kGemm, r0, hi, j);
+    for (const auto& iv : ivals) {
+      const int k0 = iv.first, q = iv.second;
+      // row regions outer: a region's GEMMs need only that region's L21 rows
+      // (plus the U12 tiles), so the first GEMMs taken are the first ready.
+      // Steps with many GEMM tasks group consecutive regions into one task
+      // (more strips per warp: the per-task latency is amortised).
+      for (int g0 = 0, g1; g0 < nreg; g0 = g1) {
+        g1 = g0 + 1;  // regions [g0, g1) form one task: at least gm.rows rows when merging
+        while (merge && q == 1 && g1 < nreg && reg[g1 - 1].second - reg[g0].first < gm.rows) ++g1;
+        const int lo = reg[g0].first, hi = reg[g1 - 1].second;
+        for (int j = r + 1; j < nt; ++j) {
+          int r0 = std::max(lo, chol ? j * T : pe);  // Cholesky: lower triangle only
+          if (q == 1 && j == r + 1) r0 = std::max(r0, pe + T);  // tile (r+1,r+1): the walker
+          // maximal runs of tiles for which [k0, k0+q) is a stage
+          for (int x = r0; x < hi;) {
+            const int i = x / T;
+            const int xe = std::min(hi, (i + 1) * T);
+            if (!is_stage(i, j, k0, q)) {
+              x = xe;
+              continue;
+            }
+            int y = xe;
+            while (y < hi && is_stage(y / T, j, k0, q)) y = std::min(hi, (y / T + 1) * T);
+            task(kGemm, x, y, j, k0, q);
+            x = y;
+          }
+        }
       }
     }
   }
@@ -1379,6 +1666,7 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   const int nt = n / bx;
   w->ntasks = static_cast<int>(tasks.size());
   w->nurgent = nurg;
+  w->chunk = chunk_depth(bx);
   w->nsteps = n / bx;
   w->cnt_bytes = (static_cast<size_t>(nt) * nt + 3) * sizeof(int);
   cudaError_t e = cudaMalloc(&w->tasks, tasks.size() * sizeof(int4));
@@ -1438,6 +1726,7 @@ cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long l
   prm.nurgent = w.nurgent;
   prm.nuw = w.nuw;
   prm.pf_mask = prefetch_mask();
+  prm.d = w.chunk;
   // measured default: Cholesky (whose bulk GEMMs feed the next step's strips
   // directly) gains 2% from publishing each strip at once, LU does not
   prm.eager_sig = [chol] {

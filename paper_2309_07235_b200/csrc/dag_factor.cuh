@@ -28,6 +28,28 @@ namespace dag {
 
 enum TaskKind : int { kDiag = 0, kTrsmL = 1, kTrsmU = 2, kGemm = 3 };
 
+// Chunked trailing updates.  A GEMM task applies the updates of q
+// consecutive panel steps [k0, k0+q) to its rows at once (C stays in
+// registers; K = q*bx), so the C round trip, the task's dependency waits and
+// its operand staging are paid once per q steps.  The steps of tile (i, j),
+// m = min(i, j) of them before its own DIAG/TRSM, are applied in
+//   nchunks(m) full chunks of d steps [c*d, (c+1)*d)   (bulk tiles), then
+//   single steps [nchunks(m)*d, m)                      (1..d of them),
+// so the last update of every tile — the one the diagonal chain waits for —
+// is always a single step.  Each chunk / single / the final op is one
+// "stage"; the tile counter counts finished rows over stages.  Per element
+// the products are accumulated in ascending step order in both cases: the
+// result is bitwise that of step-by-step updates (same DMMA sequence).
+__host__ __device__ inline int nchunks(int m, int d) { return m >= 1 ? (m - 1) / d : 0; }
+// Stages of a tile with m updates that cover the steps < s (s a chunk
+// boundary or a single step of that tile, s <= m).
+__host__ __device__ inline int stages_before(int m, int s, int d) {
+  const int nc = nchunks(m, d);
+  return s <= nc * d ? s / d : nc + (s - nc * d);
+}
+// Stages of a tile with m updates, its final DIAG/TRSM included.
+__host__ __device__ inline int stages_total(int m, int d) { return stages_before(m, m, d) + 1; }
+
 // Widest tile the persistent kernel handles (the diag block is factored by
 // the warp-register code of diag_factor.cuh, <= 64).
 constexpr int kMaxTile = 64;
@@ -49,7 +71,12 @@ bool eligible(int n, int by, int bx);
 // Host-built task list in dependency-respecting priority order
 // (int4 {kind | j << 2, k, r0, r1}).
 // Urgent queue first, then bulk; *n_urgent (may be null) gets the urgent count.
+// (int4 {kind | j << 2, k0 | q << 16, r0, r1}: GEMM tasks apply steps
+// [k0, k0 + q), every other task q = 1.)
 std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent);
+
+// Chunk depth d used for (n, by, bx) (TT_DAG_CHUNK overrides; 1 = step by step).
+int chunk_depth(int bx);
 
 struct Workspace {
   int4* tasks = nullptr;   // device task list
@@ -60,6 +87,7 @@ struct Workspace {
   int* cnt = nullptr;      // nt*nt tile counters + urgent counter, abort flag, bulk counter
   size_t cnt_bytes = 0;
   int grid = 0;
+  int chunk = 1;           // chunk depth d
   unsigned long long* trace = nullptr;  // TT_DAG_TRACE=1: per-task timestamps
   double* solve = nullptr;              // per-step diagonal reciprocals written by DIAG
 };

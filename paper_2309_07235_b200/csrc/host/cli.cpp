@@ -320,6 +320,7 @@ int cmd_tune(const Args& a) {
   int got = 0;
   double total = 0.0;
   const std::int64_t created = static_cast<std::int64_t>(std::time(nullptr));
+  std::string failure;
   if (synthetic) {
     const int rc = tt_tune_synthetic(tid, kid, s.c_str(), seed, static_cast<int>(max_evals), max_seconds,
                                      batch, rec.data(), static_cast<int>(rec.size()), &got, &total);
@@ -335,7 +336,10 @@ int cmd_tune(const Args& a) {
                                     max_seconds, devices.data(), static_cast<int>(devices.size()), warmups,
                                     reps, 0, 1, rec.data(), static_cast<int>(rec.size()), &got, &total, err,
                                     sizeof err);
-    if (rc) throw Domain(std::string("measured tuning failed: ") + err);
+    // MeasurementError: the partial trace is still written (harness.cpp:252-256
+    // flushes it before rethrowing); the error is reported after the flush
+    if (rc && !(rc == TT_EDEVICE && got > 0)) throw Domain(std::string("measured tuning failed: ") + err);
+    if (rc) failure = std::string("measured tuning failed (partial trace flushed): ") + err;
   }
 
   tth::Trace tr;
@@ -373,6 +377,7 @@ int cmd_tune(const Args& a) {
     f << tth::render_trace(tr);
     if (!f.flush()) throw Domain("write failed: " + out);
   }
+  if (!failure.empty()) throw Domain(failure);
   // report_best (tiletuner.cpp:139-151)
   std::cout << "trace: " << out << '\n' << "evals: " << tr.records.size() << '\n';
   std::vector<int> best;

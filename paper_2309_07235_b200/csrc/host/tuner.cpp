@@ -200,6 +200,37 @@ int grow(Tree& t, const Mat& x, const std::vector<double>& y, std::vector<int> i
 
 }  // namespace
 
+// Runs body(i) for i in [0, n) on up to `threads` host threads (static
+// round-robin assignment; the result of each i does not depend on the order).
+template <class F>
+void parallel_for(int n, int threads, F&& body) {
+  threads = std::max(1, std::min(threads, n));
+  if (threads == 1) {
+    for (int i = 0; i < n; ++i) body(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve(threads - 1);
+  for (int w = 1; w < threads; ++w)
+    pool.emplace_back([&, w] {
+      for (int i = w; i < n; i += threads) body(i);
+    });
+  for (int i = 0; i < n; i += threads) body(i);
+  for (auto& th : pool) th.join();
+}
+
+int host_threads() {
+  static const int n = [] {
+    const unsigned hw = std::thread::hardware_concurrency();
+    return static_cast<int>(std::max(1u, std::min(hw, 16u)));
+  }();
+  return n;
+}
+
+// surrogate.cpp:140-160.  The bootstrap samples of every tree are drawn first,
+// in tree order, from the one seeded stream — exactly the draws of the
+// sequential fit — and the trees are then grown in parallel (growing uses no
+// randomness), so the forest is the same for any thread count.
 Forest fit_forest(const Mat& x, const std::vector<double>& y, int n_trees, int max_depth,
                   int min_split, std::uint64_t seed) {
   if (x.empty() || x.size() != y.size()) throw std::invalid_argument("fit_forest: bad data");
@@ -207,13 +238,13 @@ Forest fit_forest(const Mat& x, const std::vector<double>& y, int n_trees, int m
   f.dims = static_cast<int>(x.front().size());
   Rng rng(seed);
   const int n = static_cast<int>(x.size());
-  for (int t = 0; t < n_trees; ++t) {
-    std::vector<int> idx(n);
+  std::vector<std::vector<int>> boot(n_trees, std::vector<int>(n));
+  for (auto& idx : boot)
     for (int& i : idx) i = static_cast<int>(rng.next_index(n));  // bootstrap
-    Tree tr;
-    grow(tr, x, y, std::move(idx), 0, max_depth, min_split, f.dims);
-    f.trees.push_back(std::move(tr));
-  }
+  f.trees.resize(n_trees);
+  parallel_for(n_trees, host_threads(), [&](int t) {
+    grow(f.trees[t], x, y, std::move(boot[t]), 0, max_depth, min_split, f.dims);
+  });
   return f;
 }
 
@@ -341,16 +372,23 @@ class BayesOptTuner final : public Tuner {
  protected:
   // tuners.cpp:331-351 for k = 1.  k > 1: one forest fit and one pool,
   // the k best LCB scores (ties to the lower flat index).
+  // Warm-up: random untaken configs until init_ configs have RESULTS (the
+  // reference's history_.size() < init_size_, tuners.cpp:333-335); with
+  // several evaluators in flight that can be more than init_ random asks.
+  // Never returns fewer than k unless the space is exhausted.
   std::vector<std::uint64_t> pick(int k) override {
     std::vector<std::uint64_t> out;
-    while (static_cast<int>(out.size()) < k &&
-           hist_flat_.size() + pending_.size() < static_cast<std::size_t>(init_)) {
-      out.push_back(sample_untaken());
-      pending_.insert(out.back());
+    if (hist_flat_.size() < static_cast<std::size_t>(init_)) {
+      while (static_cast<int>(out.size()) < k) {
+        const std::uint64_t f = sample_untaken();
+        if (f >= size_) break;  // exhausted
+        out.push_back(f);
+        pending_.insert(f);
+      }
+      for (auto f : out) pending_.erase(f);
+      return out;
     }
-    for (auto f : out) pending_.erase(f);
-    const int need = k - static_cast<int>(out.size());
-    if (need <= 0 || hist_flat_.empty()) return out;
+    const int need = k;
     for (auto f : out) pending_.insert(f);
     std::vector<std::uint64_t> pool = candidate_pool();
     for (auto f : out) pending_.erase(f);
@@ -359,14 +397,17 @@ class BayesOptTuner final : public Tuner {
     X.reserve(hist_flat_.size());
     for (auto f : hist_flat_) X.push_back(encode(space_, config_at(space_, f)));
     const Forest model = fit_forest(X, log_runtimes_, 25, 12, 2, seed_);
-    std::vector<std::pair<double, std::uint64_t>> scored;
-    scored.reserve(pool.size());
-    for (auto f : pool) {
-      const auto e = encode(space_, config_at(space_, f));
-      double m, sd;
-      predict_forest(model, e.data(), &m, &sd);
-      scored.push_back({m - 1.96 * sd, f});  // lcb, kappa = 1.96 (tuners.hpp:172-176)
-    }
+    std::vector<std::pair<double, std::uint64_t>> scored(pool.size());
+    const int np = static_cast<int>(pool.size());
+    const int chunks = std::min(host_threads(), std::max(1, np / 256));
+    parallel_for(chunks, chunks, [&](int c) {
+      for (int i = c; i < np; i += chunks) {
+        const auto e = encode(space_, config_at(space_, pool[i]));
+        double m, sd;
+        predict_forest(model, e.data(), &m, &sd);
+        scored[i] = {m - 1.96 * sd, pool[i]};  // lcb, kappa = 1.96 (tuners.hpp:172-176)
+      }
+    });
     if (need == 1) {  // first strict minimum over the ascending pool
       auto best = scored.front();
       for (const auto& p : scored)
@@ -398,11 +439,65 @@ std::unique_ptr<Tuner> make_tuner(TunerKind kind, const Space& space, std::uint6
 
 // ---------------------------------------------------------------- the loops
 
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double secs(Clock::time_point a, Clock::time_point b) {
+  return std::chrono::duration<double>(b - a).count();
+}
+
+// Candidates for idle evaluators.  One evaluator: ask_batch(1) per
+// evaluation, the reference's ask() (tuners.cpp:52-58) — traces stay
+// bit-identical.  W evaluators: one ask_batch(W) per refill, i.e. ONE
+// surrogate fit per W evaluations (the k best LCB scores of that fit),
+// handed out as evaluators go idle; candidates whose evaluator's device
+// failed are handed out again first.  `ask_s` accumulates the host time
+// spent asking (charged to each candidate of the batch in equal shares).
+class Proposer {
+ public:
+  Proposer(Tuner& t, int batch) : t_(t), batch_(std::max(1, batch)) {}
+
+  // next candidate (nullopt: space exhausted); `budget` caps a refill
+  std::optional<std::uint64_t> next(std::uint64_t budget, double* ask_share) {
+    *ask_share = 0.0;
+    if (!requeue_.empty()) {
+      const auto f = requeue_.front();
+      requeue_.pop_front();
+      return f;
+    }
+    if (buf_.empty()) {
+      const int k = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(batch_, budget)));
+      const auto t0 = Clock::now();
+      const auto got = t_.ask_batch(k);
+      const double dt = secs(t0, Clock::now());
+      ask_s_ += dt;
+      if (got.empty()) return std::nullopt;
+      share_ = dt / static_cast<double>(got.size());
+      buf_.assign(got.begin(), got.end());
+    }
+    const auto f = buf_.front();
+    buf_.pop_front();
+    *ask_share = share_;
+    return f;
+  }
+  void requeue(std::uint64_t f) { requeue_.push_back(f); }
+  double ask_s() const { return ask_s_; }
+
+ private:
+  Tuner& t_;
+  int batch_;
+  std::deque<std::uint64_t> buf_, requeue_;
+  double share_ = 0.0, ask_s_ = 0.0;
+};
+
+}  // namespace
+
 std::vector<Record> run_tuning_synthetic(const TuneOptions& opt, double* total_s) {
   if (opt.max_evals < 1) throw std::invalid_argument("run_tuning: max_evals must be >= 1");
   const Space space = build_space(opt.kernel, opt.size);
   auto tuner = make_tuner(opt.tuner, space, opt.seed);
   const int W = std::max(1, opt.workers);
+  Proposer prop(*tuner, W);
   // discrete-event simulation: (finish time, issue order, worker, flat)
   using Ev = std::tuple<double, std::uint64_t, int, std::uint64_t>;
   std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> running;
@@ -414,12 +509,13 @@ std::vector<Record> run_tuning_synthetic(const TuneOptions& opt, double* total_s
   auto dispatch = [&] {
     while (!idle.empty() && recs.size() + running.size() < opt.max_evals &&
            !(opt.max_seconds && now >= *opt.max_seconds)) {
-      auto got = tuner->ask_batch(1);
-      if (got.empty()) break;
+      double share;
+      const auto got = prop.next(opt.max_evals - recs.size() - running.size(), &share);
+      if (!got) break;
       const int w = idle.back();
       idle.pop_back();
-      const double rt = synthetic_objective(space, config_at(space, got[0]));
-      running.emplace(now + rt, issued++, w, got[0]);
+      const double rt = synthetic_objective(space, config_at(space, *got));
+      running.emplace(now + rt, issued++, w, *got);
     }
   };
   dispatch();
@@ -432,7 +528,7 @@ std::vector<Record> run_tuning_synthetic(const TuneOptions& opt, double* total_s
     const double rt = synthetic_objective(space, cfg);
     tuner->tell(flat, rt);
     best = std::min(best, rt);
-    recs.push_back({recs.size(), flat, cfg, rt, now, best, w});
+    recs.push_back({recs.size(), flat, cfg, rt, now, best, w, 0.0, rt});
     idle.push_back(w);
     dispatch();
   }
@@ -441,44 +537,52 @@ std::vector<Record> run_tuning_synthetic(const TuneOptions& opt, double* total_s
 }
 
 std::vector<Record> run_tuning(const TuneOptions& opt, const Objective& objective,
-                               double* total_s) {
+                               double* total_s, std::string* error) {
   if (opt.max_evals < 1) throw std::invalid_argument("run_tuning: max_evals must be >= 1");
   const Space space = build_space(opt.kernel, opt.size);
   auto tuner = make_tuner(opt.tuner, space, opt.seed);
   const int W = std::max(1, opt.workers);
-  using Clock = std::chrono::steady_clock;
+  Proposer prop(*tuner, W);
 
+  struct Job {
+    std::uint64_t flat;
+    double ask_s;
+  };
   struct Done {
     int worker;
     std::uint64_t flat;
     std::optional<double> rt;
     bool error;
     std::string what;
+    double ask_s, eval_s;
   };
   std::mutex mu;
   std::condition_variable cv;
   std::deque<Done> done;
-  std::vector<std::optional<std::uint64_t>> job(W);
+  std::vector<std::optional<Job>> job(W);
+  std::vector<bool> dead(W, false);
   bool stop = false;
 
   std::vector<std::thread> threads;
   for (int w = 0; w < W; ++w) {
     threads.emplace_back([&, w] {
       for (;;) {
-        std::uint64_t flat;
+        Job jb;
         {
           std::unique_lock<std::mutex> lk(mu);
           cv.wait(lk, [&] { return stop || job[w].has_value(); });
           if (stop && !job[w]) return;
-          flat = *job[w];
+          jb = *job[w];
         }
-        Done d{w, flat, std::nullopt, false, {}};
+        Done d{w, jb.flat, std::nullopt, false, {}, jb.ask_s, 0.0};
+        const auto t0 = Clock::now();
         try {
-          d.rt = objective(w, config_at(space, flat));
+          d.rt = objective(w, config_at(space, jb.flat));
         } catch (const std::exception& e) {
           d.error = true;
           d.what = e.what();
         }
+        d.eval_s = secs(t0, Clock::now());
         {
           std::lock_guard<std::mutex> lk(mu);
           job[w].reset();
@@ -490,21 +594,26 @@ std::vector<Record> run_tuning(const TuneOptions& opt, const Objective& objectiv
   }
 
   const auto start = Clock::now();
-  auto elapsed = [&] { return std::chrono::duration<double>(Clock::now() - start).count(); };
+  auto elapsed = [&] { return secs(start, Clock::now()); };
   std::vector<Record> recs;
   double best = std::numeric_limits<double>::infinity();
-  int in_flight = 0;
-  std::string error;
+  int in_flight = 0, alive = W;
+  std::string first_error;
+  bool exhausted = false;
   {
     std::unique_lock<std::mutex> lk(mu);
     auto dispatch = [&] {
       for (int w = 0; w < W; ++w) {
-        if (job[w] || !error.empty()) continue;
+        if (job[w] || dead[w] || exhausted) continue;
         if (recs.size() + in_flight >= opt.max_evals) return;
         if (opt.max_seconds && elapsed() >= *opt.max_seconds) return;  // checked before each eval
-        auto got = tuner->ask_batch(1);
-        if (got.empty()) return;
-        job[w] = got[0];
+        double share;
+        const auto got = prop.next(opt.max_evals - recs.size() - in_flight, &share);
+        if (!got) {
+          exhausted = true;
+          return;
+        }
+        job[w] = Job{*got, share};
         ++in_flight;
       }
     };
@@ -517,15 +626,21 @@ std::vector<Record> run_tuning(const TuneOptions& opt, const Objective& objectiv
         done.pop_front();
         --in_flight;
         if (d.error) {
-          if (error.empty()) error = d.what;
+          // MeasurementError on this evaluator's device (harness.cpp:252-256):
+          // the evaluator is retired and its candidate handed to another one;
+          // with none left the run stops and returns the partial trace.
+          if (first_error.empty()) first_error = d.what;
+          dead[d.worker] = true;
+          --alive;
+          prop.requeue(d.flat);
           continue;
         }
         tuner->tell(d.flat, d.rt);
         if (d.rt) best = std::min(best, *d.rt);
         recs.push_back({recs.size(), d.flat, config_at(space, d.flat), d.rt, elapsed(), best,
-                        d.worker});
+                        d.worker, d.ask_s, d.eval_s});
       }
-      dispatch();
+      if (alive > 0) dispatch();
       cv.notify_all();
     }
     stop = true;
@@ -533,7 +648,74 @@ std::vector<Record> run_tuning(const TuneOptions& opt, const Objective& objectiv
   cv.notify_all();
   for (auto& t : threads) t.join();
   if (total_s) *total_s = elapsed();
-  if (!error.empty()) throw std::runtime_error(error);
+  if (error) {
+    error->clear();
+    if (alive == 0) *error = first_error;  // every evaluator failed: the run is incomplete
+  } else if (alive == 0) {
+    throw std::runtime_error(first_error);
+  }
+  return recs;
+}
+
+std::vector<Record> run_tuning_virtual(const TuneOptions& opt, const VirtualObjective& objective,
+                                       double* total_s, std::string* error) {
+  if (opt.max_evals < 1) throw std::invalid_argument("run_tuning: max_evals must be >= 1");
+  const Space space = build_space(opt.kernel, opt.size);
+  auto tuner = make_tuner(opt.tuner, space, opt.seed);
+  const int W = std::max(1, opt.workers);
+  Proposer prop(*tuner, W);
+  struct Ev {
+    double fin;
+    std::uint64_t ord;
+    int worker;
+    std::uint64_t flat;
+    std::optional<double> rt;
+    double ask_s, eval_s;
+    bool operator>(const Ev& o) const { return fin != o.fin ? fin > o.fin : ord > o.ord; }
+  };
+  std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> running;
+  std::vector<Record> recs;
+  double now = 0.0, disp = 0.0, best = std::numeric_limits<double>::infinity();
+  std::uint64_t issued = 0;
+  std::vector<int> idle;
+  for (int w = W - 1; w >= 0; --w) idle.push_back(w);
+  std::string err;
+  // the dispatcher is one host thread: asks are serial on the virtual clock
+  auto dispatch = [&] {
+    while (!idle.empty() && err.empty() && recs.size() + running.size() < opt.max_evals) {
+      const double t_ask = std::max(now, disp);
+      if (opt.max_seconds && t_ask >= *opt.max_seconds) break;
+      const double before = prop.ask_s();
+      double share;
+      const auto got = prop.next(opt.max_evals - recs.size() - running.size(), &share);
+      disp = t_ask + (prop.ask_s() - before);  // the real host time of this ask
+      if (!got) break;
+      const int w = idle.back();
+      idle.pop_back();
+      std::pair<std::optional<double>, double> r;
+      try {
+        r = objective(config_at(space, *got));  // measured now, revealed at its finish time
+      } catch (const std::exception& e) {
+        err = e.what();  // the one real device failed: every virtual evaluator is gone
+        break;
+      }
+      running.push({disp + r.second, issued++, w, *got, r.first, share, r.second});
+    }
+  };
+  dispatch();
+  while (!running.empty()) {
+    Ev e = running.top();
+    running.pop();
+    now = e.fin;
+    tuner->tell(e.flat, e.rt);
+    if (e.rt) best = std::min(best, *e.rt);
+    recs.push_back({recs.size(), e.flat, config_at(space, e.flat), e.rt, now, best, e.worker,
+                    e.ask_s, e.eval_s});
+    idle.push_back(e.worker);
+    dispatch();
+  }
+  if (total_s) *total_s = now;
+  if (error) *error = err;
   return recs;
 }
 

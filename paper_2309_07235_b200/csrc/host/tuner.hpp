@@ -142,6 +142,8 @@ struct Record {
   double elapsed_s;
   double best_so_far_s;
   int worker;
+  double ask_s;   // host time spent asking for this candidate (its share of a batch ask)
+  double eval_s;  // wall time of its evaluation (objective call)
 };
 
 struct TuneOptions {
@@ -159,11 +161,28 @@ struct TuneOptions {
 // workers.  Throwing aborts the run (MeasurementError semantics).
 using Objective = std::function<std::optional<double>(int worker, const std::vector<int>& cfg)>;
 
-// Measured run: wall clock, workers evaluate concurrently, a worker asks for
-// the next candidate as soon as it is idle (no lock-step), records are
-// appended in completion order (elapsed non-decreasing, best = prefix min).
+// Measured run: wall clock, workers evaluate concurrently, an idle worker
+// gets the next candidate at once (no lock-step; with W workers the surrogate
+// is fitted once per W candidates), records are appended in completion order
+// (elapsed non-decreasing, best = prefix min).  An objective that throws
+// (MeasurementError: device failure) retires its worker and its candidate is
+// re-evaluated by another one; when no worker is left the run stops and the
+// partial trace is returned with *error set (harness.cpp:252-256 flushes the
+// partial trace and rethrows) — with error == nullptr it throws instead.
 std::vector<Record> run_tuning(const TuneOptions& opt, const Objective& objective,
-                               double* total_s);
+                               double* total_s, std::string* error = nullptr);
+
+// Virtual-clock measured run (T1 / T8 harness): `workers` evaluators emulated
+// on ONE real device.  Every evaluation is measured for real — the objective
+// returns (runtime or nullopt, wall seconds the evaluation took) — and
+// occupies its virtual evaluator for that wall time; the dispatcher's real
+// host ask time is charged serially on the same clock.  Results reach the
+// tuner at their virtual finish time, so the search sees exactly what a
+// W-GPU run with these per-evaluation costs would see.
+using VirtualObjective =
+    std::function<std::pair<std::optional<double>, double>(const std::vector<int>& cfg)>;
+std::vector<Record> run_tuning_virtual(const TuneOptions& opt, const VirtualObjective& objective,
+                                       double* total_s, std::string* error);
 
 // Synthetic run (harness.cpp:166-197, virtual clock): `workers` simulated
 // devices, discrete-event completion order by virtual finish time.  With

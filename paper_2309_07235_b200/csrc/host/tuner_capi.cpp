@@ -1,5 +1,8 @@
 // C ABI of the host tuning runtime (include/tt_tuner.h).
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -55,6 +58,8 @@ void fill(const std::vector<Record>& recs, tt_record* out, int cap, int* n_out) 
     r.elapsed_s = recs[i].elapsed_s;
     r.best_so_far_s = recs[i].best_so_far_s;
     r.worker = recs[i].worker;
+    r.ask_s = recs[i].ask_s;
+    r.eval_s = recs[i].eval_s;
   }
 }
 
@@ -213,11 +218,46 @@ int tt_tune_synthetic(int tuner, int kernel, const char* size, uint64_t seed, in
   });
 }
 
+namespace {
+
+// TT_FAULT_INJECT="w:n": worker w fails (MeasurementError) at its n-th evaluation.
+struct FaultPlan {
+  int worker = -1, at = -1;
+};
+FaultPlan fault_plan() {
+  FaultPlan f;
+  if (const char* v = std::getenv("TT_FAULT_INJECT")) std::sscanf(v, "%d:%d", &f.worker, &f.at);
+  return f;
+}
+
+void copy_err(const std::string& msg, char* err, int errcap) {
+  if (err && errcap > 0) {
+    std::strncpy(err, msg.c_str(), static_cast<size_t>(errcap) - 1);
+    err[errcap - 1] = '\0';
+  }
+}
+
+TuneOptions options(int tuner, Kernel k, const char* size, uint64_t seed, int max_evals,
+                    double max_seconds, int workers) {
+  TuneOptions o;
+  o.tuner = static_cast<TunerKind>(tuner);
+  o.kernel = k;
+  o.size = size;
+  o.seed = seed;
+  o.max_evals = static_cast<std::uint64_t>(max_evals);
+  if (max_seconds > 0) o.max_seconds = max_seconds;
+  o.workers = workers;
+  return o;
+}
+
+}  // namespace
+
 int tt_tune_measured(int tuner, int kernel, const char* size, uint64_t seed, uint64_t input_seed,
                      int max_evals, double max_seconds, const int* devices, int n_devices,
                      int warmups, int reps, int aggregate, int spot, tt_record* out, int cap,
                      int* n_out, double* total_s, char* err, int errcap) {
   std::string msg;
+  if (n_out) *n_out = 0;
   const int rc = guarded(
       [&] {
         if (n_devices < 1) throw std::invalid_argument("need at least one device");
@@ -249,30 +289,70 @@ int tt_tune_measured(int tuner, int kernel, const char* size, uint64_t seed, uin
         for (auto& t : th) t.join();
         for (auto& e : errs)
           if (!e.empty()) throw std::runtime_error(e);
-        TuneOptions o;
-        o.tuner = static_cast<TunerKind>(tuner);
-        o.kernel = k;
-        o.size = size;
-        o.seed = seed;
-        o.max_evals = static_cast<std::uint64_t>(max_evals);
-        if (max_seconds > 0) o.max_seconds = max_seconds;
-        o.workers = n_devices;
+        const FaultPlan fp = fault_plan();
+        std::vector<int> evals(n_devices, 0);  // per worker (each touched by its own thread)
         Objective obj = [&](int w, const std::vector<int>& cfg) -> std::optional<double> {
+          if (w == fp.worker && evals[w]++ == fp.at)
+            throw std::runtime_error("injected device fault on worker " + std::to_string(w));
           double secs = 0.0;
           const int r = tt_measure(ctxs[w].h, cfg.data(), static_cast<int>(cfg.size()), warmups,
                                    reps, aggregate, &secs);
           if (r == TT_ENUMERIC) return std::nullopt;  // penalised failure (harness.cpp:250-251)
-          check(ctxs[w].h, r, "measure");              // MeasurementError aborts the run
+          check(ctxs[w].h, r, "measure");              // MeasurementError: worker retired
           return secs;
         };
-        fill(run_tuning(o, obj, total_s), out, cap, n_out);
+        std::string run_err;
+        const auto recs = run_tuning(options(tuner, k, size, seed, max_evals, max_seconds, n_devices),
+                                     obj, total_s, &run_err);
+        fill(recs, out, cap, n_out);  // the (partial) trace is returned either way
+        if (!run_err.empty()) throw std::runtime_error("measurement error: " + run_err);
         return TT_OK;
       },
       &msg);
-  if (rc != TT_OK && err && errcap > 0) {
-    std::strncpy(err, msg.c_str(), static_cast<size_t>(errcap) - 1);
-    err[errcap - 1] = '\0';
-  }
+  if (rc != TT_OK) copy_err(msg, err, errcap);
+  return rc;
+}
+
+int tt_tune_virtual(int tuner, int kernel, const char* size, uint64_t seed, uint64_t input_seed,
+                    int max_evals, double max_seconds, int device, int n_virtual, int warmups,
+                    int reps, int aggregate, int spot, tt_record* out, int cap, int* n_out,
+                    double* total_s, char* err, int errcap) {
+  std::string msg;
+  if (n_out) *n_out = 0;
+  const int rc = guarded(
+      [&] {
+        if (n_virtual < 1) throw std::invalid_argument("need at least one evaluator");
+        if (warmups < 0 || reps < 1)
+          throw std::invalid_argument("measure: warmups must be >= 0 and repetitions >= 1");
+        const Kernel k = kernel_of(kernel);
+        const ProblemSize* ps = find_size(k, size);
+        if (!ps) throw std::out_of_range(std::string("unregistered problem size: ") + size);
+        Ctx c;
+        if (tt_ctx_create(device, &c.h) != TT_OK)
+          throw std::runtime_error("tt_ctx_create failed on device " + std::to_string(device));
+        if (spot) spot_check(c.h, k);
+        check(c.h, tt_setup_seeded(c.h, kernel, ps->n, ps->l, ps->m, ps->o, ps->p, input_seed),
+              "setup");
+        VirtualObjective obj = [&](const std::vector<int>& cfg) {
+          const auto t0 = std::chrono::steady_clock::now();
+          double secs = 0.0;
+          const int r = tt_measure(c.h, cfg.data(), static_cast<int>(cfg.size()), warmups, reps,
+                                   aggregate, &secs);
+          const double wall =
+              std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+          if (r == TT_ENUMERIC) return std::make_pair(std::optional<double>(), wall);
+          check(c.h, r, "measure");
+          return std::make_pair(std::optional<double>(secs), wall);
+        };
+        std::string run_err;
+        const auto recs = run_tuning_virtual(
+            options(tuner, k, size, seed, max_evals, max_seconds, n_virtual), obj, total_s, &run_err);
+        fill(recs, out, cap, n_out);
+        if (!run_err.empty()) throw std::runtime_error("measurement error: " + run_err);
+        return TT_OK;
+      },
+      &msg);
+  if (rc != TT_OK) copy_err(msg, err, errcap);
   return rc;
 }
 

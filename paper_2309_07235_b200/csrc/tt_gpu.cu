@@ -1016,6 +1016,11 @@ int tt_dag_tasks(int kernel, int n, int by, int bx, int* out, int cap) {
   return static_cast<int>(v.size());
 }
 
+int tt_dag_chunk_depth(int n, int by, int bx) {
+  if (!tt::dag::eligible(n, by, bx)) return -1;
+  return tt::dag::chunk_depth(bx);
+}
+
 int tt_dag_urgent(int kernel, int n, int by, int bx) {
   if (!tt::dag::eligible(n, by, bx)) return -1;
   int nu = 0;

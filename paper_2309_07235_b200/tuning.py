@@ -21,7 +21,8 @@ class Record(ctypes.Structure):
     _fields_ = [("eval_index", ctypes.c_uint64), ("flat", ctypes.c_uint64),
                 ("config", ctypes.c_int * 6), ("nconfig", ctypes.c_int), ("failed", ctypes.c_int),
                 ("runtime_s", ctypes.c_double), ("elapsed_s", ctypes.c_double),
-                ("best_so_far_s", ctypes.c_double), ("worker", ctypes.c_int)]
+                ("best_so_far_s", ctypes.c_double), ("worker", ctypes.c_int),
+                ("ask_s", ctypes.c_double), ("eval_s", ctypes.c_double)]
 
 
 @dataclass
@@ -33,6 +34,8 @@ class EvalRecord:
     elapsed_s: float
     best_so_far_s: float
     worker: int
+    ask_s: float = 0.0
+    eval_s: float = 0.0
 
 
 _lib_t = None
@@ -62,6 +65,9 @@ def load():
     L.tt_tune_measured.argtypes = [c_int, c_int, cp, u64, u64, c_int, dbl, vp, c_int, c_int, c_int,
                                    c_int, c_int, vp, c_int, ctypes.POINTER(c_int),
                                    ctypes.POINTER(dbl), ctypes.c_char_p, c_int]
+    L.tt_tune_virtual.argtypes = [c_int, c_int, cp, u64, u64, c_int, dbl, c_int, c_int, c_int, c_int,
+                                  c_int, c_int, vp, c_int, ctypes.POINTER(c_int),
+                                  ctypes.POINTER(dbl), ctypes.c_char_p, c_int]
     _lib_t = L
     return L
 
@@ -163,7 +169,7 @@ def _records(buf, n) -> list[EvalRecord]:
         r = buf[i]
         out.append(EvalRecord(r.eval_index, r.flat, tuple(r.config[:r.nconfig]),
                               None if r.failed else r.runtime_s, r.elapsed_s, r.best_so_far_s,
-                              r.worker))
+                              r.worker, r.ask_s, r.eval_s))
     return out
 
 
@@ -196,8 +202,56 @@ def run_tuning_measured(tuner: str, kernel: str, size: str, seed: int, max_evals
                                  1 if spot_check else 0, ctypes.cast(buf, ctypes.c_void_p),
                                  max_evals, ctypes.byref(n), ctypes.byref(tot), err, 512)
     if rc:
-        raise RuntimeError(f"run_tuning (measured) failed ({rc}): {err.value.decode()}")
+        raise TuningError(f"run_tuning (measured) failed ({rc}): {err.value.decode()}",
+                          _records(buf, n.value))
     return _records(buf, n.value), tot.value
+
+
+class TuningError(RuntimeError):
+    """MeasurementError during a measured run; `records` holds the flushed partial trace
+    (harness.cpp:252-256)."""
+
+    def __init__(self, msg: str, records):
+        super().__init__(msg)
+        self.records = records
+
+
+def run_tuning_virtual(tuner: str, kernel: str, size: str, seed: int, max_evals: int,
+                       workers: int, device: int = 0, max_seconds: float | None = None,
+                       warmups: int = 1, reps: int = 3, aggregate: str = "median",
+                       spot_check: bool = True, input_seed: int = 1):
+    """T1/T8 harness: `workers` evaluators emulated on one real device (virtual clock;
+    every evaluation measured for real, host ask time charged serially)."""
+    buf = (Record * max_evals)()
+    n = ctypes.c_int()
+    tot = ctypes.c_double()
+    err = ctypes.create_string_buffer(512)
+    rc = load().tt_tune_virtual(TUNERS[tuner], KERNELS[kernel], size.encode(), seed, input_seed,
+                                max_evals, max_seconds or 0.0, device, workers, warmups, reps,
+                                _lib.AGGREGATES[aggregate], 1 if spot_check else 0,
+                                ctypes.cast(buf, ctypes.c_void_p), max_evals, ctypes.byref(n),
+                                ctypes.byref(tot), err, 512)
+    if rc:
+        raise TuningError(f"run_tuning (virtual) failed ({rc}): {err.value.decode()}",
+                          _records(buf, n.value))
+    return _records(buf, n.value), tot.value
+
+
+def time_to_reach(records, best_runtime: float, best_flat: int | None = None) -> float:
+    """elapsed_s of the first record with runtime <= best_runtime or that
+    evaluates the same configuration (best_flat)."""
+    for r in records:
+        if (r.runtime_s is not None and r.runtime_s <= best_runtime) or \
+                (best_flat is not None and r.flat == best_flat):
+            return r.elapsed_s
+    return float("inf")
+
+
+def best_record(records):
+    """First record achieving the run's final best (its time is T1 for a 1-GPU run)."""
+    ok = [r for r in records if r.runtime_s is not None]
+    best = min(r.runtime_s for r in ok)
+    return next(r for r in ok if r.runtime_s == best)
 
 
 def time_to_best(records, target: float | None = None) -> float:

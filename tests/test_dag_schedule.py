@@ -30,44 +30,68 @@ CASES = [("lu", 64, 8, 8), ("lu", 64, 16, 8), ("lu", 96, 3, 12), ("lu", 120, 40,
 
 
 def decode(t):
-    return int(t[0]) & 3, int(t[0]) >> 2, int(t[1]), int(t[2]), int(t[3])
+    """{kind | j << 2, k0 | q << 16, r0, r1}: a GEMM applies steps [k0, k0+q)."""
+    return int(t[0]) & 3, int(t[0]) >> 2, int(t[1]) & 0xFFFF, max(1, int(t[1]) >> 16), \
+        int(t[2]), int(t[3])
 
 
 def tiles(r0, r1, T):
     return range(r0 // T, (r1 - 1) // T + 1)
 
 
-def needs(kind, j, k, r0, r1, T, chol):
-    kT = k * T
+def stages_before(m, s, d):
+    """dag_factor.cuh: stages of a tile with m updates covering the steps < s
+    (nchunks(m) full chunks of d steps, then single steps)."""
+    nc = (m - 1) // d if m >= 1 else 0
+    return s // d if s <= nc * d else nc + (s - nc * d)
+
+
+def fin(m, d):
+    return stages_before(m, m, d) + 1
+
+
+def ready(t):
+    kind, _, k0, q, _, _ = decode(t)
+    return k0 + q - 1 if kind == GEMM else k0
+
+
+def needs(kind, j, k0, q, r0, r1, T, chol, d, full=False):
+    """What the kernel waits on (dep_at / strip_deps).  A GEMM over [k0, kl] waits
+    only for the operands of step kl; full=True lists every step's operands,
+    which the chain argument (dag_factor.cu, dep_at) says are then final too."""
     if kind == DIAG:
-        return [((k, k), kT)]
+        return [((k0, k0), stages_before(k0, k0 - 1, d) * T)]
     if kind == TRSM_L:
-        return [((i, k), kT) for i in tiles(r0, r1, T)] + [((k, k), kT + T)]
+        return [((i, k0), stages_before(k0, k0, d) * T) for i in tiles(r0, r1, T)] + \
+            [((k0, k0), fin(k0, d) * T)]
     if kind == TRSM_U:
-        return [((k, j), kT), ((k, k), kT + T)]
+        return [((k0, j), stages_before(k0, k0, d) * T), ((k0, k0), fin(k0, d) * T)]
+    kl = k0 + q - 1
+    ks = range(k0, kl + 1) if full else [kl]
     out = []
     for i in tiles(r0, r1, T):
-        out += [((i, j), kT), ((i, k), kT + T)]
-    return out + [((j, k) if chol else (k, j), kT + T)]
+        out.append(((i, j), stages_before(min(i, j), k0, d) * T))
+        out += [((i, k), fin(k, d) * T) for k in ks]
+    return out + [(((j, k) if chol else (k, j)), fin(k, d) * T) for k in ks]
 
 
-def signals(kind, j, k, r0, r1, T):
+def signals(kind, j, k0, r0, r1, T):
     if kind == DIAG:
-        return {(k, k): T}
+        return {(k0, k0): T}
     if kind == TRSM_U:
-        return {(k, j): T}
-    col = k if kind == TRSM_L else j
+        return {(k0, j): T}
+    col = k0 if kind == TRSM_L else j
     return {(i, col): min(r1, (i + 1) * T) - max(r0, i * T) for i in tiles(r0, r1, T)}
 
 
-def walker_needs(k, T, nt, chol):
+def walker_needs(k, T, nt, chol, d):
     out = []
-    if k >= 2:
-        out.append(((k, k), (k - 1) * T))
+    if k >= 1:
+        out.append(((k, k), stages_before(k, k - 1, d) * T))
     if k + 1 < nt:
-        out.append(((k + 1, k), k * T))
+        out.append(((k + 1, k), stages_before(k, k, d) * T))
         if not chol:
-            out.append(((k, k + 1), k * T))
+            out.append(((k, k + 1), stages_before(k, k, d) * T))
     return out
 
 
@@ -80,33 +104,35 @@ def walker_signals(k, T, nt, chol):
     return sig
 
 
-def interleaved(tasks, nt, T, chol, nurg):
+def interleaved(tasks, nt, T, chol, nurg, d):
     """A sequential execution the kernel's queues admit: per step k the walker,
-    then step k of the urgent queue, then step k of the bulk queue, each queue
-    in its own order.  Every wait condition must hold when its task is
-    reached; together with the per-queue step order this is the kernel's
-    deadlock-freedom argument (see build_tasks)."""
+    then the urgent tasks of ready step k, then the bulk tasks of ready step k,
+    each queue in its own order.  Every wait condition (and every operand of a
+    chunked GEMM) must hold when its task is reached; together with the
+    per-queue ready-step order this is the kernel's deadlock-freedom argument
+    (see build_tasks)."""
     urg, bulk = tasks[:nurg], tasks[nurg:]
     for q in (urg, bulk):
-        assert np.all(np.diff(q[:, 1]) >= 0), "queue not in step order"
+        rs = [ready(t) for t in q]
+        assert all(x <= y for x, y in zip(rs, rs[1:])), "queue not in ready-step order"
     cnt = np.zeros((nt, nt), dtype=np.int64)
     out = []
     iu = ib = 0
     for k in range(nt):
-        for tile, nd in walker_needs(k, T, nt, chol):
+        for tile, nd in walker_needs(k, T, nt, chol, d):
             assert cnt[tile] >= nd, ("walker", k, tile, nd, cnt[tile])
         out.append(("W", k))
         for tile, rows in walker_signals(k, T, nt, chol).items():
             cnt[tile] += rows
         for q, idx in ((urg, "u"), (bulk, "b")):
             i = iu if idx == "u" else ib
-            while i < len(q) and q[i][1] == k:
+            while i < len(q) and ready(q[i]) == k:
                 t = q[i]
-                kind, j, kk, r0, r1 = decode(t)
-                for tile, nd in needs(kind, j, kk, r0, r1, T, chol):
+                kind, j, k0, qq, r0, r1 = decode(t)
+                for tile, nd in needs(kind, j, k0, qq, r0, r1, T, chol, d, full=True):
                     assert cnt[tile] >= nd, (idx, t, tile, nd, cnt[tile])
                 out.append(("Q", t))
-                for tile, rows in signals(kind, j, kk, r0, r1, T).items():
+                for tile, rows in signals(kind, j, k0, r0, r1, T).items():
                     cnt[tile] += rows
                 i += 1
             if idx == "u":
@@ -123,15 +149,16 @@ def test_task_order_and_coverage(kernel, n, by, bx):
     assert tasks is not None
     chol = kernel == "cholesky"
     T, nt = bx, n // bx
+    d = _lib.dag_chunk_depth(n, by, bx)
     assert not np.any((tasks[:, 0] & 3) == DIAG)  # DIAG belongs to the walker
     cnt = np.zeros((nt, nt), dtype=np.int64)
     nurg = _lib.load().tt_dag_urgent(_lib.KERNEL_IDS[kernel], n, by, bx)
-    for what, t in interleaved(tasks, nt, T, chol, nurg):
+    for what, t in interleaved(tasks, nt, T, chol, nurg, d):
         if what == "W":
-            need, sig = walker_needs(t, T, nt, chol), walker_signals(t, T, nt, chol)
+            need, sig = walker_needs(t, T, nt, chol, d), walker_signals(t, T, nt, chol)
         else:
-            kind, j, k, r0, r1 = decode(t)
-            need, sig = needs(kind, j, k, r0, r1, T, chol), signals(kind, j, k, r0, r1, T)
+            kind, j, k0, q, r0, r1 = decode(t)
+            need, sig = needs(kind, j, k0, q, r0, r1, T, chol, d), signals(kind, j, k0, r0, r1, T)
         for (tile, nd) in need:
             assert cnt[tile] >= nd, (what, t, tile, nd, cnt[tile])
         for tile, rows in sig.items():
@@ -139,24 +166,35 @@ def test_task_order_and_coverage(kernel, n, by, bx):
             if chol:
                 assert i >= jj, t
             cnt[tile] += rows
-            assert cnt[tile] <= (min(i, jj) + 1) * T, (what, t, tile)
+            assert cnt[tile] <= fin(min(i, jj), d) * T, (what, t, tile)
     for i in range(nt):
         for jj in range(nt):
             if chol and jj > i:
                 assert cnt[i, jj] == 0
             else:
-                assert cnt[i, jj] == (min(i, jj) + 1) * T, (i, jj)
+                assert cnt[i, jj] == fin(min(i, jj), d) * T, (i, jj)
 
 
-def run_tasks_numpy(a, tasks, bx, chol, nurg):
+def test_chunked_updates_present():
+    """Bulk tiles get their updates d steps at a time (K = d * bx)."""
+    for kernel, n, by, bx in (("cholesky", 4000, 250, 50), ("lu", 4000, 160, 50), ("lu", 2000, 200, 40)):
+        tasks = _lib.dag_tasks(kernel, n, by, bx)
+        d = _lib.dag_chunk_depth(n, by, bx)
+        assert d >= 4
+        qs = tasks[:, 1] >> 16
+        gem = (tasks[:, 0] & 3) == GEMM
+        assert np.any(qs[gem] == d) and np.all((qs[gem] == 1) | (qs[gem] == d))
+
+
+def run_tasks_numpy(a, tasks, bx, chol, nurg, d):
     a = a.copy()
     T = bx
     nt = a.shape[0] // T
 
     def trsm_l(k, r0, r1):
         kT = k * T
-        d = a[kT:kT + T, kT:kT + T]
-        m = np.tril(d).T if chol else np.triu(d)
+        dd = a[kT:kT + T, kT:kT + T]
+        m = np.tril(dd).T if chol else np.triu(dd)
         a[r0:r1, kT:kT + T] = np.linalg.solve(m.T, a[r0:r1, kT:kT + T].T).T
 
     def trsm_u(k, j):
@@ -164,22 +202,25 @@ def run_tasks_numpy(a, tasks, bx, chol, nurg):
         lo = np.tril(a[kT:kT + T, kT:kT + T], -1) + np.eye(T)
         a[kT:kT + T, jT:jT + T] = np.linalg.solve(lo, a[kT:kT + T, jT:jT + T])
 
-    def gemm(k, r0, r1, j):
-        kT, jT = k * T, j * T
-        b = a[jT:jT + T, kT:kT + T].T if chol else a[kT:kT + T, jT:jT + T]
-        upd = a[r0:r1, jT:jT + T] - a[r0:r1, kT:kT + T] @ b
+    def gemm(k0, q, r0, r1, j):
+        jT = j * T
+        c = a[r0:r1, jT:jT + T].copy()
+        for k in range(k0, k0 + q):  # ascending steps, as the kernel accumulates them
+            kT = k * T
+            b = a[jT:jT + T, kT:kT + T].T if chol else a[kT:kT + T, jT:jT + T]
+            c = c - a[r0:r1, kT:kT + T] @ b
         if chol:
             rows = np.arange(r0, r1)[:, None]
             cols = np.arange(jT, jT + T)[None, :]
-            upd = np.where(rows >= cols, upd, a[r0:r1, jT:jT + T])
-        a[r0:r1, jT:jT + T] = upd
+            c = np.where(rows >= cols, c, a[r0:r1, jT:jT + T])
+        a[r0:r1, jT:jT + T] = c
 
-    for what, t in interleaved(tasks, nt, T, chol, nurg):
+    for what, t in interleaved(tasks, nt, T, chol, nurg, d):
         if what == "W":  # walker step k
             k = t
             kT = k * T
             if k >= 1:
-                gemm(k - 1, kT, kT + T, k)
+                gemm(k - 1, 1, kT, kT + T, k)
             blk = a[kT:kT + T, kT:kT + T].copy()
             if chol:
                 oracle.cholesky_factor_inplace(blk, T, T)
@@ -192,14 +233,32 @@ def run_tasks_numpy(a, tasks, bx, chol, nurg):
                 if not chol:
                     trsm_u(k, k + 1)
             continue
-        kind, j, k, r0, r1 = decode(t)
+        kind, j, k0, q, r0, r1 = decode(t)
         if kind == TRSM_L:
-            trsm_l(k, r0, r1)
+            trsm_l(k0, r0, r1)
         elif kind == TRSM_U:
-            trsm_u(k, j)
+            trsm_u(k0, j)
         else:
-            gemm(k, r0, r1, j)
+            gemm(k0, q, r0, r1, j)
     return a
+
+
+# forced chunk depths (TT_DAG_CHUNK): many tiles per chunk at small n
+CHUNKED = [("lu", 120, 40, 8, 3), ("lu", 160, 32, 16, 2), ("lu", 96, 3, 8, 4), ("lu", 200, 50, 10, 5),
+           ("cholesky", 128, 16, 8, 4), ("cholesky", 160, 40, 10, 3), ("cholesky", 96, 96, 8, 2),
+           ("cholesky", 200, 5, 8, 6), ("lu", 64, 64, 8, 1), ("cholesky", 64, 8, 8, 1)]
+
+
+@pytest.mark.parametrize("kernel,n,by,bx,d", CHUNKED)
+def test_chunked_order_coverage_and_semantics(monkeypatch, kernel, n, by, bx, d):
+    monkeypatch.setenv("TT_DAG_CHUNK", str(d))
+    assert _lib.dag_chunk_depth(n, by, bx) == d
+    test_task_order_and_coverage(kernel, n, by, bx)
+    test_task_semantics_reproduce_reference(kernel, n, by, bx)
+    tasks = _lib.dag_tasks(kernel, n, by, bx)
+    gem = (tasks[:, 0] & 3) == GEMM
+    if d > 1 and n // bx > d + 1:
+        assert np.any((tasks[gem, 1] >> 16) == d)
 
 
 @pytest.mark.parametrize("kernel,n,by,bx", [c for c in CASES if c[1] <= 160])
@@ -207,7 +266,8 @@ def test_task_semantics_reproduce_reference(kernel, n, by, bx):
     chol = kernel == "cholesky"
     a0 = oracle.gen_spd(n, 5)
     nurg = _lib.load().tt_dag_urgent(_lib.KERNEL_IDS[kernel], n, by, bx)
-    out = run_tasks_numpy(a0, _lib.dag_tasks(kernel, n, by, bx), bx, chol, nurg)
+    out = run_tasks_numpy(a0, _lib.dag_tasks(kernel, n, by, bx), bx, chol, nurg,
+                          _lib.dag_chunk_depth(n, by, bx))
     ref = a0.copy()
     if chol:
         oracle.cholesky_factor_inplace(ref, by, bx)

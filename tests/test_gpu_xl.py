@@ -150,7 +150,7 @@ def test_mm3_xl_vs_oracle(gpu_ctx, cache, cfg):
 def test_huge_pivots_divide_exactly(gpu_ctx, kernel):
     """Pivots beyond 2^1022 (1/pivot subnormal): the reference divides exactly
     (kernels.cpp:191, :293-295); the GPU's reciprocal seed must not flush to 0."""
-    a = oracle.gen_spd(64, 1) * 2.0 ** 1011  # diagonal ~ 2^1022.4 .. 2^1023
+    a = oracle.gen_spd(64, 1) * 2.0 ** 1016  # diagonal ~ 85 * 2^1016 ~ 2^1022.4
     assert np.max(np.abs(np.diag(a))) > 2.0 ** 1022
     for cfg in ((8, 8), (16, 32), (64, 64), (32, 16)):
         ref = a.copy()

@@ -1,5 +1,6 @@
 """CPU tests of the host tuning runtime (libtt_tuner.so): bit-exact search space,
 reference-identical k=1 tuning traces, and the batch extension's invariants."""
+import numpy as np
 import pytest
 
 from paper_2309_07235_b200 import tuning
@@ -111,3 +112,36 @@ def test_budget_max_seconds():
     recs, tot = tuning.run_tuning_synthetic("random", "lu", "large", 1, 400, max_seconds=50.0)
     assert 0 < len(recs) < 400
     assert recs[-2].elapsed_s < 50.0  # checked before each evaluation
+
+
+def test_bayesopt_warmup_with_pending_never_empty():
+    """Warm-up counts configurations with RESULTS (tuners.cpp:333-335): with more
+    evaluators in flight than the warm-up size the tuner keeps handing out random
+    untaken configurations instead of an empty (= exhausted) batch."""
+    t = tuning.Tuner("bayesopt", "lu", "large", 3)  # init = max(4, 2*2) = 4
+    first = t.ask_batch(8)
+    assert len(first) == 8 and len(set(first)) == 8
+    more = t.ask_batch(3)  # still no results: random again, never empty
+    assert len(more) == 3 and not set(more) & set(first)
+    for f in first[:4]:
+        t.tell(f, 1.0 + f * 1e-3)
+    model = t.ask_batch(4)  # 4 results: the surrogate takes over (one fit, top-4 LCB)
+    assert len(model) == 4 and not set(model) & set(first + more)
+
+
+def test_batch_ask_one_fit_per_batch_is_fast():
+    """One surrogate fit per batch (parallel trees): a 3mm XL ask over 200 results
+    stays far below the ~20 ms a 3mm XL evaluation takes on the GPU."""
+    import time
+    t = tuning.Tuner("bayesopt", "3mm", "extralarge", 5)
+    rng = np.random.default_rng(0)
+    told = 0
+    while told < 200:
+        for f in t.ask_batch(8):
+            t.tell(f, float(rng.random()))
+            told += 1
+    t0 = time.perf_counter()
+    got = t.ask_batch(8)
+    dt = time.perf_counter() - t0
+    assert len(got) == 8
+    assert dt < 0.2, dt  # one fit + 2048-point scoring for 8 candidates

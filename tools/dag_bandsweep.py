@@ -16,4 +16,4 @@ fl = (2 / 3 if kern == "lu" else 1 / 3) * n ** 3
 import os
 print(json.dumps({"kernel": kern, "n": n, "by": by, "bx": bx, "band": os.environ.get("TT_DAG_BAND"),
                   "ucta": os.environ.get("TT_DAG_URGENT_CTAS"),
-                  "pf": os.environ.get("TT_DAG_PREFETCH"), "ms": s * 1e3, "tflops": fl / s / 1e12}))
+                  "pf": os.environ.get("TT_DAG_PREFETCH"), "chunk": os.environ.get("TT_DAG_CHUNK"), "merge": os.environ.get("TT_DAG_MERGE"), "ms": s * 1e3, "tflops": fl / s / 1e12}))
