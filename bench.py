@@ -1,32 +1,40 @@
 #!/usr/bin/env python3
-"""Benchmark: fp64 GFLOP/s of the tuned kernels on B200 (BASELINE.json metric).
+"""Benchmark: fp64 GFLOP/s of the best-tuned config (% of B200 fp64 peak); tuning
+time-to-best (BASELINE.json metric).
 
-Headline workload (configs[1]): LU without pivoting, PolyBench LARGE N=2000,
-fixed block (by, bx) = BENCH_LU_BLOCK, inputs gen_spd(2000, seed=1).  A step
-is one in-place factorisation of one resident input matrix: ONE launch of the
-persistent tile-DAG kernel (paper_2309_07235_b200/csrc/dag_factor.cu; walker
-CTA on the diagonal chain + queue workers on the bulk TRSM/GEMM tasks).  Inputs cycle
-through a ring of W+K distinct device copies (each step's input is cold in
-L2: the ring is W+K x 32 MB and every copy was written during setup), so
-there is no restore copy in the timed region.
+Headline workload (configs[2]): Cholesky, PolyBench EXTRALARGE N=4000, at the
+BO-tuned knob setting BENCH_CHOL_BLOCK = (by, bx) — the best configuration of the
+committed 1-GPU BayesOpt run (seed TUNE_SEED, TUNE_EVALS evaluations,
+profiles/tune_chol_xl_r02.json) — inputs gen_spd(4000, seed=1).  A step is one
+in-place factorisation of one resident input: ONE launch of the persistent
+tile-DAG kernel (paper_2309_07235_b200/csrc/dag_factor.cu).  Inputs cycle through
+a ring of W+K distinct device copies (128 MB each: larger than the 126 MB L2, so
+every step starts L2-cold), no restore copy inside the timed region.
 
-value   = algorithmic (2/3) n^3 flop per step x steps x ranks / max-over-ranks
-          device time (CUDA events on the launching stream)
-e2e     = same metric through the C ABI with pinned host buffers (H2D + factor
-          + D2H every step): tt_lu_factor_batch, the pipelined batch of the
-          drop-in; the per-call drop-in tt_lu_factor_inplace is e2e.single_call
-roofline: bound "tensor" (fp64 DMMA); the dominant (only) kernel of a step
-          is the persistent factorisation kernel, so achieved = (2/3) n^3 per
-          launch / its CUDA-event launch time; peak = the measured DMMA issue
-          rate on this pool's B200s (profiles/fp64_peak_r01.jsonl, 37.05
-          TFLOP/s; MEASURED_PEAKS.json has no fp64 entry); traffic = DRAM
-          bytes of one ncu --set full capture (profiles/ncu_traffic.json).
-Multi-GPU: LU is single-GPU per factorisation (north_star), so N ranks run
-N independent replicas ("replicas only", scaling "weak").
+value    = (1/3) n^3 flop per step x steps x ranks / max-over-ranks device time
+           (CUDA events on the launching stream)
+tuning   = a LIVE 1-GPU BayesOpt run in this process (same seed / budget as the
+           committed one): time_to_best_s = elapsed_s of its first record reaching
+           its final best, plus the config it found (SURVEY 8e definition)
+e2e      = the same metric through the C ABI with pinned host buffers (H2D +
+           factor + D2H every step): tt_cholesky_factor_batch, the pipelined batch
+           drop-in; the one-call-per-matrix tt_cholesky_factor_inplace beside it
+roofline : bound "tensor" (fp64 DMMA); the dominant (only) kernel of a step is the
+           persistent factorisation kernel: achieved = (1/3) n^3 per launch / its
+           CUDA-event time; peak = the measured DMMA issue rate on this pool's
+           B200s (profiles/fp64_peak_r01.jsonl, 37.05 TFLOP/s; MEASURED_PEAKS.json
+           has no fp64 entry); traffic = DRAM bytes of one ncu --set full capture
+           (profiles/ncu_traffic.json)
+cpu_baseline: the unmodified reference core (oracle/_ref) factoring the same
+           input at the same (by, bx) on 1 host thread (one factorisation)
+extra    : the other BASELINE configs (LU LARGE fixed block, LU XL, 3mm LARGE fixed
+           tile, 3mm XL), each with its own roofline
+Multi-GPU: a factorisation is single-GPU (north_star), so N ranks run N
+independent replicas ("replicas only", scaling "weak").
 
-`--impl reference` times the reference's own CPU implementation (the
-unmodified core compiled into oracle/_ref by oracle/Makefile, else the C
-port) on all host cores, each thread factoring its own copy.
+`--impl reference` times the reference's own CPU implementation (the unmodified
+core compiled into oracle/_ref by oracle/Makefile, else the C port) on all host
+cores, each thread factoring its own copy, on the same config.
 """
 from __future__ import annotations
 
@@ -46,9 +54,19 @@ sys.path.insert(0, str(ROOT))
 
 FP64_PEAK_TFLOPS = 37.05  # measured DMMA m8n8k4 issue rate (profiles/fp64_peak_r01.jsonl)
 FP64_PEAK_SOURCE = "measured: DMMA issue-rate microbenchmark, 148 SMs @1965 MHz (profiles/fp64_peak_r01.jsonl); cuBLAS DGEMM 8192^3 = 35.45"
-BENCH_N = 2000
-BENCH_LU_BLOCK = (200, 40)  # (by, bx): fastest fixed block of the N=2000 knob sweep of the final round-1 kernel (profiles/sweep_lu2000_r01c.jsonl: 0.879 ms; (250,50) 0.930, the paper's A100 best (400,50) 1.000)
 METRIC = "fp64 GFLOP/s of best-tuned config (% of B200 fp64 peak); tuning time-to-best"
+BENCH_N = 4000
+BENCH_CHOL_BLOCK = (250, 40)  # (by, bx): best of the committed BO run (profiles/tune_chol_xl_r02.json)
+TUNE_SEED = 1
+TUNE_EVALS = 60
+WORKLOAD = "cholesky_extralarge_bo_tuned"
+
+
+def bench_config():
+    """The config dict both arms print (identical keys and values)."""
+    by, bx = BENCH_CHOL_BLOCK
+    return {"workload": WORKLOAD, "kernel": "cholesky", "n": BENCH_N, "by": by, "bx": bx,
+            "tuner": "bayesopt", "tuning_seed": TUNE_SEED, "tuning_evals": TUNE_EVALS}
 
 
 def lu_flops(n: int) -> float:
@@ -157,60 +175,60 @@ def max_over_ranks(x: float, world: int) -> float:
 
 # ------------------------------------------------------------------ CPU arms
 
-def cpu_reference_lu(n: int, by: int, bx: int, steps: int, threads: int, budget_s: float):
-    """Reference CPU LU on `threads` host threads (one matrix each per step)."""
+def _ref_factor(ref, buf, by, bx):
     import oracle
-    ref = oracle.ref_lib()
-    kind = "reference" if ref is not None else "port"
-    base = oracle.gen_spd(n, 1)  # bitwise gen_spd(n, 1)
-    pristine = [base.copy() for _ in range(threads)]
-
-    def factor(buf):
-        if ref is not None:
-            rc = ref.ref_lu_factor_inplace(buf.ctypes.data_as(ctypes.c_void_p), n, n, by, bx)
-        else:
-            rc = 0
-            oracle.lu_factor_inplace(buf, by, bx)
-        assert rc == 0
-
-    times = []
-    t_start = time.perf_counter()
-    for _ in range(steps):
-        work = [p.copy() for p in pristine]
-        ths = [threading.Thread(target=factor, args=(w,)) for w in work]
-        t0 = time.perf_counter()
-        for t in ths:
-            t.start()
-        for t in ths:
-            t.join()
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_start > budget_s:
-            break
-    return kind, times
+    n = buf.shape[0]
+    if ref is not None:
+        rc = ref.ref_cholesky_factor_inplace(buf.ctypes.data_as(ctypes.c_void_p), n, n, by, bx)
+        assert rc == 0, ref.ref_last_error()
+    else:
+        oracle.cholesky_factor_inplace(buf, by, bx)
 
 
 def run_reference_arm(args, rank, world):
+    """The reference CPU implementation on all host threads, one matrix per thread."""
     if rank != 0:
         return
-    by, bx = BENCH_LU_BLOCK
+    import oracle
+    by, bx = BENCH_CHOL_BLOCK
+    ref = oracle.ref_lib()
+    kind = "reference" if ref is not None else "port"
     threads = os.cpu_count() or 1
-    # bounded: one warm-up step, then up to K steps within ~150 s of CPU time
-    kind, warm = cpu_reference_lu(BENCH_N, by, bx, 1 if args.warmup > 0 else 0, threads, 60.0) \
-        if args.warmup > 0 else ("reference", [])
-    kind, times = cpu_reference_lu(BENCH_N, by, bx, args.steps, threads, 150.0)
+    t0 = time.perf_counter()
+    base = oracle.gen_spd(BENCH_N, 1)  # bitwise gen_spd(4000, 1)
+    gen_s = time.perf_counter() - t0
+
+    def step():
+        work = [base.copy() for _ in range(threads)]
+        ths = [threading.Thread(target=_ref_factor, args=(ref, w, by, bx)) for w in work]
+        t = time.perf_counter()
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        return time.perf_counter() - t
+
+    if args.warmup > 0:
+        step()  # one warm-up step (bounded)
+    times, budget = [], 150.0
+    t_start = time.perf_counter()
+    for _ in range(args.steps):
+        times.append(step())
+        if time.perf_counter() - t_start > budget:
+            break
     total = sum(times)
-    value = threads * lu_flops(BENCH_N) * len(times) / total / 1e9
+    value = threads * chol_flops(BENCH_N) * len(times) / total / 1e9
     sample = (f"{len(times)} step(s) x {threads} threads, each thread one in-place "
-              f"lu_factor_inplace(gen_spd({BENCH_N},1), by={by}, bx={bx}); "
-              f"{'unmodified reference core (oracle/_ref)' if kind == 'reference' else 'C port (oracle/tt_oracle.c)'}")
+              f"cholesky_factor_inplace(gen_spd({BENCH_N},1), by={by}, bx={bx}); "
+              f"{'unmodified reference core (oracle/_ref)' if kind == 'reference' else 'C port (oracle/tt_oracle.c)'}"
+              f"; input generation ({gen_s:.1f} s) untimed")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": len(times), "steps_requested": args.steps,
-        "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3,
+        "warmup": 1 if args.warmup > 0 else 0, "ms_per_step": total / len(times) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (gen_spd(2000, seed=1), bitwise the reference generator)",
-        "config": {"workload": f"lu_nopiv_large_n{BENCH_N}_fixed_block", "n": BENCH_N,
-                   "by": by, "bx": bx, "threads": threads},
+        "data": "synthetic (gen_spd(4000, seed=1), bitwise the reference generator)",
+        "config": bench_config(),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
@@ -219,38 +237,42 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_single(n, by, bx):
-    """Reference measure() protocol (1 warm-up + median of 3) on 1 core."""
+def cpu_baseline_single(a, by, bx):
+    """The reference core factoring the same input at the same knobs, 1 host thread."""
     import oracle
     ref = oracle.ref_lib()
-    if ref is not None:
-        cfg = (ctypes.c_int * 2)(by, bx)
-        out = ctypes.c_double()
-        t0 = time.perf_counter()
-        rc = ref.ref_measure(0, b"large", 1, ctypes.cast(cfg, ctypes.c_void_p), 2, 1, 3, 0,
-                             ctypes.byref(out))
-        assert rc == 0, ref.ref_last_error()
-        wall = time.perf_counter() - t0
-        secs = out.value
-        kind = "reference"
-        sample = (f"reference measure(KernelCase{{lu/large, seed 1}}, ({by},{bx}), protocol 1 "
-                  f"warm-up + median of 3) on 1 host thread; {wall:.1f} s incl. gen_spd")
-    else:
-        a = oracle.gen_spd(n, 1)
-        ts = []
-        for _ in range(4):
-            w = a.copy()
-            t0 = time.perf_counter()
-            oracle.lu_factor_inplace(w, by, bx)
-            ts.append(time.perf_counter() - t0)
-        secs = float(np.median(ts[1:]))
-        kind = "port"
-        sample = f"C port lu_factor_inplace n={n} ({by},{bx}), 1 warm-up + median of 3, 1 thread"
-    return {"value": lu_flops(n) / secs / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": kind,
+    w = a.copy()
+    t0 = time.perf_counter()
+    _ref_factor(ref, w, by, bx)
+    secs = time.perf_counter() - t0
+    kind = "reference" if ref is not None else "port"
+    n = a.shape[0]
+    sample = (f"one cholesky_factor_inplace(gen_spd({n},1), by={by}, bx={bx}) on 1 host thread "
+              f"({'unmodified reference core, oracle/_ref' if kind == 'reference' else 'C port'}); "
+              f"input downloaded from the device generator (bitwise gen_spd)")
+    return {"value": chol_flops(n) / secs / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": kind,
             "sample": sample, "seconds_per_factorisation": secs}
 
 
 # ------------------------------------------------------------------ GPU arm
+
+def live_tuning(local):
+    """1-GPU BayesOpt on the headline case: time-to-best and the config found."""
+    from paper_2309_07235_b200 import tuning
+    t0 = time.perf_counter()
+    recs, total = tuning.run_tuning_measured("bayesopt", "cholesky", "extralarge", TUNE_SEED,
+                                             TUNE_EVALS, devices=(local,))
+    wall = time.perf_counter() - t0
+    best = tuning.best_record(recs)
+    return {"tuner": "bayesopt", "seed": TUNE_SEED, "evals": len(recs), "devices": 1,
+            "protocol": "reference measure(): 1 warm-up + median of 3, CUDA events",
+            "time_to_best_s": best.elapsed_s, "tuning_s": total, "wall_s_incl_setup": wall,
+            "best_config": list(best.config), "best_ms": best.runtime_s * 1e3,
+            "best_pct_of_fp64_peak": 100 * chol_flops(BENCH_N) / best.runtime_s / 1e12 / FP64_PEAK_TFLOPS,
+            "host_ask_s_total": sum(r.ask_s for r in recs),
+            "committed_config": list(BENCH_CHOL_BLOCK),
+            "found_committed_config": list(best.config) == list(BENCH_CHOL_BLOCK)}
+
 
 def run_gpu_arm(args, rank, world, local):
     import torch
@@ -258,19 +280,22 @@ def run_gpu_arm(args, rank, world, local):
     from paper_2309_07235_b200 import _lib
 
     torch.cuda.set_device(local)
+    tuning = live_tuning(local) if (rank == 0 and world == 1 and not args.no_tuning) else None
     ctx = Context(local)
     lib = ctx.lib
     n = BENCH_N
-    by, bx = BENCH_LU_BLOCK
-    ld = n  # 2000 is a multiple of 16: rows already 128-byte aligned
-    # one explicit stream shared by torch (events, copies) and the library
-    stream = torch.cuda.Stream(device=local)
+    by, bx = BENCH_CHOL_BLOCK
+    ld = n  # 4000 is a multiple of 16: rows already 128-byte aligned
+    stream = torch.cuda.Stream(device=local)  # shared by torch (events, copies) and the library
     torch.cuda.set_stream(stream)
     sptr = ctypes.c_void_p(stream.cuda_stream)
 
-    # inputs: gen_spd(2000, 1) generated on the device (bitwise the reference's)
-    runner = GpuKernelRunner(KernelCase("lu", n, seed=1), ctx)
+    # inputs: gen_spd(4000, 1) generated on the device (bitwise the reference's)
+    runner = GpuKernelRunner(KernelCase("cholesky", n, seed=1), ctx)
     (host_a,) = runner.inputs()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_single(host_a, by, bx)  # GPU idle meanwhile
     base = torch.from_numpy(host_a).to(f"cuda:{local}")
     ring_len = args.warmup + args.steps
     ring = torch.empty((ring_len, n, ld), dtype=torch.float64, device=f"cuda:{local}")
@@ -278,19 +303,15 @@ def run_gpu_arm(args, rank, world, local):
     torch.cuda.synchronize()
 
     def factor(i):
-        rc = lib.tt_dev_lu(ctx.handle, ctypes.c_void_p(ring[i].data_ptr()), n, ld, by, bx, None,
-                           sptr)
-        ctx.check(rc)
+        ctx.check(lib.tt_dev_cholesky(ctx.handle, ctypes.c_void_p(ring[i].data_ptr()), n, ld, by,
+                                      bx, None, sptr))
 
-    # Instantiation cache: a schedule's CUDA graph is specific to its buffer,
-    # so build the graph of every ring entry first (untimed), then restore the
-    # pristine inputs and evict them from L2 with a 256 MB write.
+    # the instantiation cache holds one graph per buffer: build them all (untimed),
+    # then restore the pristine inputs
     for i in range(ring_len):
         factor(i)
     torch.cuda.synchronize()
     ring.copy_(base.expand(ring_len, n, ld))
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
-    flush.fill_(1)
     torch.cuda.synchronize()
     for i in range(args.warmup):
         factor(i)
@@ -309,82 +330,89 @@ def run_gpu_arm(args, rank, world, local):
     ms = e0.elapsed_time(e1)
     launches_timed = ctx.launches - launches_w
     ms_max = max_over_ranks(ms, world)
-    value = world * args.steps * lu_flops(n) / (ms_max * 1e-3) / 1e9
+    value = world * args.steps * chol_flops(n) / (ms_max * 1e-3) / 1e9
 
-    # correctness of the timed outputs (size-independent property): residual of the last factor
-    check = torch.empty_like(base)
-    check.copy_(ring[ring_len - 1])
-    torch.cuda.synchronize()
+    # correctness of a timed output against the input (numpy BLAS as the checker)
+    out_last = ring[ring_len - 1].cpu().numpy()
+    del ring
+    torch.cuda.empty_cache()
 
     # e2e through the C ABI with pinned host buffers: the pipelined batch entry
-    # (tt_lu_factor_batch: H2D / factorisation / D2H of neighbouring matrices
-    # overlap) is the headline; the per-call drop-in (tt_lu_factor_inplace,
-    # one synchronous round trip per matrix) is reported beside it.
-    e2e_steps = max(4, min(args.steps, 20))
+    # (H2D / factorisation / D2H of neighbouring matrices overlap) is the headline;
+    # the per-call drop-in (one synchronous round trip per matrix) beside it
+    e2e_steps = 8
     host = [torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
-            for _ in range(e2e_steps + 1)]
+            for _ in range(e2e_steps)]
     for h in host:
         h[...] = host_a
-    idx = ctypes.c_int(-1)
-    ctx.check(lib.tt_lu_factor_inplace(ctx.handle, _lib.ptr(host[-1]), n, n, by, bx,
-                                       ctypes.byref(idx)))  # warm the one-shot graph
-    ptrs = (ctypes.c_void_p * e2e_steps)(*[h.ctypes.data for h in host[:e2e_steps]])
+    ptrs = (ctypes.c_void_p * e2e_steps)(*[h.ctypes.data for h in host])
     fails = (ctypes.c_int * e2e_steps)()
-    # warm-up: the same batch call as the timed one (graphs, streams, status slots)
-    ctx.check(lib.tt_lu_factor_batch(ctx.handle, ptrs, e2e_steps, n, by, bx, fails))
-    for h in host[:e2e_steps]:
+    ctx.check(lib.tt_cholesky_factor_batch(ctx.handle, ptrs, e2e_steps, n, by, bx, fails))  # warm
+    for h in host:
         h[...] = host_a
     barrier(world)
     t0 = time.perf_counter()
-    ctx.check(lib.tt_lu_factor_batch(ctx.handle, ptrs, e2e_steps, n, by, bx, fails))
+    ctx.check(lib.tt_cholesky_factor_batch(ctx.handle, ptrs, e2e_steps, n, by, bx, fails))
     e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-    e2e_value = world * e2e_steps * lu_flops(n) / e2e_s / 1e9
-    single = [torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy() for _ in range(4)]
+    e2e_value = world * e2e_steps * chol_flops(n) / e2e_s / 1e9
+    single = host[:2]
+    for h in single:
+        h[...] = host_a
+    idx = ctypes.c_int(-1)
+    ctx.check(lib.tt_cholesky_factor_inplace(ctx.handle, _lib.ptr(single[0]), n, n, by, bx,
+                                             ctypes.byref(idx)))  # warm the one-shot graph
     for h in single:
         h[...] = host_a
     barrier(world)
     t0 = time.perf_counter()
     for h in single:
-        ctx.check(lib.tt_lu_factor_inplace(ctx.handle, _lib.ptr(h), n, n, by, bx,
-                                           ctypes.byref(idx)))
+        ctx.check(lib.tt_cholesky_factor_inplace(ctx.handle, _lib.ptr(h), n, n, by, bx,
+                                                 ctypes.byref(idx)))
     single_s = max_over_ranks(time.perf_counter() - t0, world)
-    single_value = world * len(single) * lu_flops(n) / single_s / 1e9
+    single_value = world * len(single) * chol_flops(n) / single_s / 1e9
 
     line = None
     if rank == 0:
-        import oracle
-        res = oracle.lu_residual_packed(host_a, host[e2e_steps - 1])  # CPU check of one e2e output
-        same = bool(np.array_equal(host[0], single[0]))  # batch and per-call outputs agree bitwise
-        ref_fac = host_a.copy()
-        achieved = lu_flops(n) / (ms / args.steps * 1e-3) / 1e12
-        traffic = ncu_traffic(f"lu_nopiv_large_n{n}_fixed_block")
-        sched = schedule_info(lib, n, by, bx)
+        import numpy as np
+        l_dev = np.tril(out_last)
+        res = float(np.max(np.abs(l_dev @ l_dev.T - host_a)) / np.max(np.abs(host_a)))
+        iu = np.triu_indices(n, 1)
+        upper_ok = bool(np.array_equal(out_last[iu], host_a[iu]))
+        same = bool(np.array_equal(host[e2e_steps - 1], single[0]))
+        achieved = chol_flops(n) / (ms / args.steps * 1e-3) / 1e12
+        sched = schedule_info(lib, 1, n, by, bx)
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: gen_spd(2000, seed=1) generated on the device, bitwise equal to the reference generator",
-            "config": {"workload": f"lu_nopiv_large_n{n}_fixed_block", "n": n, "by": by, "bx": bx,
-                       "parallelism": f"replicas{world}",
-                       "l2_policy": f"ring of {ring_len} distinct resident inputs (32 MB each), 256 MB L2 flush after restoring them; every timed step's input is cold in L2"},
+            "data": "synthetic: gen_spd(4000, seed=1) generated on the device, bitwise equal to the reference generator",
+            "config": bench_config(),
+            "parallelism": f"replicas{world}",
+            "l2_policy": f"ring of {ring_len} distinct resident inputs (128 MB each, larger than the 126 MB L2); every timed step's input is L2-cold",
             "pct_of_fp64_peak": 100.0 * achieved / FP64_PEAK_TFLOPS,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                         "traffic": traffic,
+                         "traffic": ncu_traffic(WORKLOAD),
                          "kernel": sched["kernel"],
-                         "launch_unit": "one launch = one full factorisation ((2/3) n^3 flop); timed with CUDA events on the launching stream",
+                         "launch_unit": "one launch = one full factorisation ((1/3) n^3 flop); timed with CUDA events on the launching stream",
                          "peak_source": FP64_PEAK_SOURCE},
             "schedule": sched,
+            "tuning": tuning,
+            "time_to_best_s": tuning["time_to_best_s"] if tuning else None,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": n * n * 8,
                     "d2h_bytes_per_step": n * n * 8, "steps": e2e_steps,
-                    "api": "tt_lu_factor_batch (C ABI, pipelined batch of lu_factor_inplace)",
+                    "api": "tt_cholesky_factor_batch (C ABI, pipelined batch of cholesky_factor_inplace)",
                     "single_call": {"value": single_value, "unit": "GFLOP/s", "steps": len(single),
-                                    "api": "tt_lu_factor_inplace (C ABI drop-in for lu_factor_inplace)"}},
+                                    "api": "tt_cholesky_factor_inplace (C ABI drop-in for cholesky_factor_inplace)"}},
             "gpu_launches": int(launches_timed),
             "clocks": clk.summary(),
-            "parity": {"lu_residual_e2e_output": res, "tolerance": 1e-12,
-                       "batch_equals_single_call": same, "ok": bool(res <= 1e-12 and same)},
+            "parity": {"cholesky_residual_timed_output": res, "tolerance": 1e-12,
+                       "upper_triangle_untouched": upper_ok,
+                       "batch_equals_single_call": same,
+                       "ok": bool(res <= 1e-12 and same and upper_ok)},
         }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
     return line, ctx
 
 
@@ -398,46 +426,49 @@ def ncu_traffic(workload: str):
         return None
 
 
-def schedule_info(lib, n, by, bx):
+def schedule_info(lib, kid, n, by, bx):
     """Which schedule the knob setting runs on (persistent DAG or launch graph)."""
-    ntasks = lib.tt_dag_tasks(0, n, by, bx, None, 0)
+    ntasks = lib.tt_dag_tasks(kid, n, by, bx, None, 0)
     if ntasks < 0:
         return {"kind": "graph", "kernel": "panel/trsm/dgemm graph (schedules.cu)"}
-    nt = n // bx
-    return {"kind": "persistent tile-DAG", "kernel": f"dag_kernel<{(bx + 7) // 8}, LU>",
-            "queue_tasks": ntasks, "urgent_tasks": lib.tt_dag_urgent(0, n, by, bx),
-            "walker_steps": nt}
+    return {"kind": "persistent tile-DAG", "kernel": f"dag_kernel<{(bx + 7) // 8}, {'CHOL' if kid else 'LU'}>",
+            "queue_tasks": ntasks, "urgent_tasks": lib.tt_dag_urgent(kid, n, by, bx),
+            "walker_steps": n // bx, "chunk_depth": lib.tt_dag_chunk_depth(n, by, bx)}
 
 
-def by_fit(extent, f):
-    """Largest divisor of `extent` not above f (the trailing view need not be divisible)."""
-    f = min(f, extent)
-    while extent % f:
-        f -= 1
-    return f
+EXTRA_CASES = [
+    # (name, kernel case args, config, flops, how the config was chosen)
+    ("lu_large_fixed_block", ("lu", 2000), (200, 40), lu_flops(2000),
+     "configs[1]: fixed block, the fastest of the N=2000 knob sweep"),
+    ("lu_extralarge", ("lu", 4000), (250, 40), lu_flops(4000), "best of the N=4000 sweep"),
+    ("mm3_large_fixed_tile", ("3mm", 800, 900, 1000, 1100, 1200), (100, 125, 125, 120, 32, 60),
+     mm3_flops(800, 900, 1000, 1100, 1200), "configs[0]: fixed tile config (grid search)"),
+    ("mm3_extralarge", ("3mm", 1600, 1800, 2000, 2200, 2400), (64, 125, 125, 300, 64, 240),
+     mm3_flops(1600, 1800, 2000, 2200, 2400), "grid-searched config"),
+]
 
 
-def extra_workloads(ctx, quick: bool):
-    """The other BASELINE configs, device-resident, CUDA-event timed (median of reps)."""
+def extra_workloads(ctx):
+    """The other BASELINE configs, device-resident, CUDA-event timed (reference
+    measure() protocol: restore copy outside the event pair, median), each with
+    its roofline against the same fp64 peak."""
     from paper_2309_07235_b200 import GpuKernelRunner, KernelCase, MeasureProtocol
     out = {}
-    proto = MeasureProtocol(2, 5, "median")
-    cases = [
-        # fixed tile configs: best of the coordinate grid search (profiles/sweep3mm_grid_r01.txt)
-        ("mm3_large_fixed", KernelCase("3mm", 800, 900, 1000, 1100, 1200), (100, 125, 125, 120, 32, 60),
-         mm3_flops(800, 900, 1000, 1100, 1200)),
-        ("mm3_extralarge", KernelCase("3mm", 1600, 1800, 2000, 2200, 2400), (64, 125, 125, 300, 64, 240),
-         mm3_flops(1600, 1800, 2000, 2200, 2400)),
-        ("cholesky_extralarge", KernelCase("cholesky", 4000), (250, 50), chol_flops(4000)),
-        ("lu_extralarge", KernelCase("lu", 4000), (160, 50), lu_flops(4000)),
-    ]
-    for name, kase, cfg, flops in cases:
+    proto = MeasureProtocol(2, 7, "median")
+    for name, kase, cfg, flops, why in EXTRA_CASES:
         try:
-            r = GpuKernelRunner(kase, ctx)
+            r = GpuKernelRunner(KernelCase(*kase), ctx)
             secs = r.measure(cfg, proto)
             tf = flops / secs / 1e12
+            kid = {"lu": 0, "cholesky": 1}.get(kase[0], 2)
             out[name] = {"config": list(cfg), "ms": secs * 1e3, "gflops": tf * 1e3,
-                         "pct_of_fp64_peak": 100 * tf / FP64_PEAK_TFLOPS}
+                         "pct_of_fp64_peak": 100 * tf / FP64_PEAK_TFLOPS, "chosen": why,
+                         "roofline": {"bound": "tensor", "achieved": tf, "peak": FP64_PEAK_TFLOPS,
+                                      "unit": "TFLOP/s", "frac": tf / FP64_PEAK_TFLOPS,
+                                      "traffic": ncu_traffic(name)},
+                         "schedule": schedule_info(ctx.lib, kid, kase[1], *cfg) if kid < 2 else
+                         {"kind": "3 DMMA GEMMs (E || F on two streams, then G)"},
+                         "timing": "median of 7 after 2 warm-ups (reference measure() protocol, CUDA events)"}
         except Exception as e:  # report, never hide
             out[name] = {"error": str(e)}
     return out
@@ -451,6 +482,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-tuning", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: at least 3 warm-up steps
@@ -458,17 +490,15 @@ def main():
 
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
         return
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_single(BENCH_N, *BENCH_LU_BLOCK)  # before the GPU phase
     line, ctx = run_gpu_arm(args, rank, world, local)
     if rank == 0:
-        if cpu is not None:
-            line["cpu_baseline"] = cpu
         if not args.no_extra and world == 1:
-            line["extra"] = extra_workloads(ctx, quick=True)
+            line["extra"] = extra_workloads(ctx)
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

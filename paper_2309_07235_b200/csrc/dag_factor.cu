@@ -539,9 +539,15 @@ __device__ void gemm_task(const Params& p, int j, int k0, int q, int r0, int r1,
     }
     double2 a[kMF][NF];
     load_a(a, ra, nr, k0);
+    // Register budget: -C (4NF doubles) + A (4NF) + the next step's A in
+    // flight (4NF).  For NF >= 7 that no longer fits next to the rest of the
+    // kernel without spills, so wide tiles load each step's A when it starts
+    // (the other warp of the SM sub-partition hides the latency).
+    constexpr bool kPrefetch = NF <= 6;
     for (int kk = 0; kk < q; ++kk) {
       double2 an[kMF][NF];
-      if (kk + 1 < q) load_a(an, ra, nr, k0 + kk + 1);
+      if (!kPrefetch && kk > 0) load_a(a, ra, nr, k0 + kk);
+      if (kPrefetch && kk + 1 < q) load_a(an, ra, nr, k0 + kk + 1);
       if (first_done && lane == 0 && kk == 0) first_done[1] = globaltimer();
       const double* B = Bs + kk * Tp * NPB;
 #pragma unroll
@@ -580,7 +586,7 @@ __device__ void gemm_task(const Params& p, int j, int k0, int q, int r0, int r1,
         warp_signal(p, prev_ra, prev_ra + prev_nr, j);
         prev_ra = -1;
       }
-      if (kk + 1 < q) {
+      if (kPrefetch && kk + 1 < q) {
 #pragma unroll
         for (int mf = 0; mf < kMF; ++mf)
 #pragma unroll
@@ -1535,11 +1541,11 @@ int prefetch_mask() {
 
 // TT_DAG_MERGE="rows,thresh": steps with >= thresh GEMM region-tasks group
 // consecutive row regions into GEMM tasks of >= rows rows (rows 0: off).
-// Default 750,250: measured on B200 over LU N=2000/4000 and Cholesky N=4000
-// (profiles/dag_merge_sweep_r01.txt) — early steps, where the bulk queue is
-// throughput-bound, get 3-6 strips per warp instead of 1-2.
+// Round 1 (step-by-step updates) used 750,250 (profiles/dag_merge_sweep_r01.txt);
+// with chunked bulk updates (K = d*bx) merging measured slower, so the
+// default is off (profiles/chunk_sweep_r02.txt).
 struct GemmMerge {
-  int rows = 750;
+  int rows = 0;  // off: with chunked bulk updates merging measured slower (profiles/chunk_sweep_r02.txt)
   long long thresh = 250;
 };
 GemmMerge gemm_merge() {
@@ -1570,29 +1576,41 @@ int chunk_depth(int bx) {
   return std::max(1, std::min({d, cap, 0xFFFF / 2}));
 }
 
-// Two queues, each in "ready step" order.  A task's ready step is the last
-// panel step whose output it reads (TRSM_L/U(k): k; a GEMM over steps
-// [k0, k0+q): k0+q-1); per ready step r the queues hold TRSM_L(r), TRSM_U(r, j),
-// then the single-step GEMMs of step r, then (when r+1 closes a chunk) the
-// chunked GEMMs of steps [r+1-d, r+1).  The urgent queue (served by a few
-// dedicated CTAs) holds what the walker needs next — the L21 rows of tile
-// rows <= r+band and the U / GEMM pieces of tile columns <= r+band above the
-// carve row (r+1+band)*bx; the bulk queue holds the rest.  Deadlock-free:
-// every task waits only on tasks of earlier ready steps, walker steps <= its
-// own, same-step tasks earlier in its own queue (TRSM before GEMM), or (bulk
-// only) same-step urgent tasks — an urgent task never reads a same-step bulk
-// task's output (its rows and columns lie inside the band); walker step r+1
-// waits only on tasks of ready steps <= r.  Row regions are `by` rows (the
-// reference's trailing row tile, kernels.cpp:205-216) aligned to multiples
-// of by and clipped to the trailing rows; a GEMM region is further split at
-// the tiles where the (chunk / single step) stage structure changes
-// (dag_factor.cuh).  Returns urgent ++ bulk; *n_urgent = urgent count.
+// Two queues.  Every task has a ready step — the last panel step whose output
+// it reads (TRSM_L/U(k): k; a GEMM over steps [k0, k0+q): k0+q-1) — and a
+// deadline — the earliest ready step of any task (or walker step) consuming
+// its output: TRSM(k): k; a single-step GEMM at step s: s+1; a chunk: the
+// next chunk's ready step, or for a tile's last chunk its first single step
+// (dag_factor.cuh).  Each queue is sorted by the key (deadline, ready step,
+// TRSM before GEMM), generation order breaking ties.  A producer Y of a
+// consumer X has deadline(Y) <= ready(X) <= deadline(X), equal keys only for
+// a same-step TRSM -> GEMM pair, so the key order is a topological order of
+// the task DAG, and the walker's step k consumes only tasks with deadline
+// <= k while every task waiting on walker step k has ready step >= k:
+// deadlock-free with in-order queues for any number of CTAs (the earliest
+// unfinished task in key order always has its inputs done and is taken next
+// in its queue).  The deadline order lets the queues serve what the diagonal
+// chain needs next first: a chunk burst (every d steps) no longer delays the
+// single-step updates of the next panel columns.
+//
+// The urgent queue (served by a few dedicated CTAs) holds what the walker
+// needs next — the L21 rows of tile rows <= r+band and the U / GEMM pieces of
+// tile columns <= r+band above the carve row (r+1+band)*bx — the bulk queue
+// the rest.  Row regions are `by` rows (the reference's trailing row tile,
+// kernels.cpp:205-216) aligned to multiples of by and clipped to the trailing
+// rows; a GEMM region is further split at the tiles where the (chunk /
+// single step) stage structure changes (dag_factor.cuh).
+// Returns urgent ++ bulk; *n_urgent = urgent count.
 std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
   const int T = bx, nt = n / bx;
   const int d = chunk_depth(bx);
   const int band = urgent_band();
   const GemmMerge gm = gemm_merge();
-  std::vector<int4> urg, bulk;
+  struct Keyed {
+    int dl, ready, kind;
+    int4 t;
+  };
+  std::vector<Keyed> urg, bulk;
   bulk.reserve(static_cast<size_t>(count_tasks(chol, n, by, bx)));
   // is [k0, k0+q) one stage of tile (i, j)?
   auto is_stage = [&](int i, int jj, int k0, int q) {
@@ -1600,25 +1618,33 @@ std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
     if (q == d && k0 % d == 0 && k0 + d <= nc * d) return true;  // a full chunk
     return q == 1 && k0 >= nc * d && k0 < m;                      // a single step
   };
+  // earliest ready step of the next stage of tile (i, j) after [k0, k0+q)
+  auto deadline = [&](int i, int jj, int k0, int q) {
+    if (q == 1) return k0 + 1;
+    const int nc = nchunks(std::min(i, jj), d), c = k0 / d;
+    return c + 1 < nc ? (c + 2) * d - 1 : nc * d;
+  };
   for (int r = 0; r + 1 < nt; ++r) {
     const int pe = (r + 1) * T;
     const int carve = std::min(n, (r + 1 + band) * T);  // rows above: tile rows <= r+band
-    auto task = [&](int kind, int r0, int r1, int j, int k0, int q) {
+    auto task = [&](int kind, int r0, int r1, int j, int k0, int q, int dl) {
       if (r0 >= r1) return;
       const int y = k0 | (q << 16);
+      const int ko = kind == kGemm ? 1 : 0;
       const bool near = kind == kTrsmU ? j <= r + band : (kind == kTrsmL || j <= r + band);
       if (near && r0 < carve) {  // split at the carve row
-        urg.push_back(make_int4(kind | (j << 2), y, r0, kind == kTrsmU ? r1 : std::min(r1, carve)));
-        if (kind != kTrsmU && r1 > carve) bulk.push_back(make_int4(kind | (j << 2), y, carve, r1));
+        urg.push_back({dl, r, ko, make_int4(kind | (j << 2), y, r0, kind == kTrsmU ? r1 : std::min(r1, carve))});
+        if (kind != kTrsmU && r1 > carve)
+          bulk.push_back({dl, r, ko, make_int4(kind | (j << 2), y, carve, r1)});
       } else {
-        bulk.push_back(make_int4(kind | (j << 2), y, r0, r1));
+        bulk.push_back({dl, r, ko, make_int4(kind | (j << 2), y, r0, r1)});
       }
     };
     std::vector<std::pair<int, int>> reg;  // row regions: multiples of by, clipped
     for (int x = (pe / by) * by; x < n; x += by) reg.emplace_back(std::max(x, pe), std::min(n, x + by));
-    for (const auto& rg : reg) task(kTrsmL, std::max(rg.first, pe + T), rg.second, 0, r, 1);  // row r+1: walker
+    for (const auto& rg : reg) task(kTrsmL, std::max(rg.first, pe + T), rg.second, 0, r, 1, r);  // row r+1: walker
     if (!chol)
-      for (int j = r + 2; j < nt; ++j) task(kTrsmU, 0, 1, j, r, 1);
+      for (int j = r + 2; j < nt; ++j) task(kTrsmU, 0, 1, j, r, 1, r);
     // GEMM intervals ready at step r: the single step r, then the chunk
     // [r+1-d, r+1) when r+1 closes one
     std::vector<std::pair<int, int>> ivals{{r, 1}};
@@ -1629,8 +1655,8 @@ std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
       const int k0 = iv.first, q = iv.second;
       // row regions outer: a region's GEMMs need only that region's L21 rows
       // (plus the U12 tiles), so the first GEMMs taken are the first ready.
-      // Steps with many GEMM tasks group consecutive regions into one task
-      // (more strips per warp: the per-task latency is amortised).
+      // Steps with many GEMM tasks may group consecutive regions into one
+      // task (TT_DAG_MERGE; off by default).
       for (int g0 = 0, g1; g0 < nreg; g0 = g1) {
         g1 = g0 + 1;  // regions [g0, g1) form one task: at least gm.rows rows when merging
         while (merge && q == 1 && g1 < nreg && reg[g1 - 1].second - reg[g0].first < gm.rows) ++g1;
@@ -1646,18 +1672,33 @@ std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
               x = xe;
               continue;
             }
-            int y = xe;
-            while (y < hi && is_stage(y / T, j, k0, q)) y = std::min(hi, (y / T + 1) * T);
-            task(kGemm, x, y, j, k0, q);
+            int y = xe, dl = deadline(i, j, k0, q);
+            while (y < hi && is_stage(y / T, j, k0, q)) {
+              dl = std::min(dl, deadline(y / T, j, k0, q));
+              y = std::min(hi, (y / T + 1) * T);
+            }
+            task(kGemm, x, y, j, k0, q, dl);
             x = y;
           }
         }
       }
     }
   }
+  auto order = [](std::vector<Keyed>& v) {
+    std::stable_sort(v.begin(), v.end(), [](const Keyed& a, const Keyed& b) {
+      if (a.dl != b.dl) return a.dl < b.dl;
+      if (a.ready != b.ready) return a.ready < b.ready;
+      return a.kind < b.kind;
+    });
+  };
+  order(urg);
+  order(bulk);
+  std::vector<int4> out;
+  out.reserve(urg.size() + bulk.size());
+  for (const auto& k : urg) out.push_back(k.t);
+  for (const auto& k : bulk) out.push_back(k.t);
   if (n_urgent) *n_urgent = static_cast<int>(urg.size());
-  urg.insert(urg.end(), bulk.begin(), bulk.end());
-  return urg;
+  return out;
 }
 
 cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {

@@ -104,42 +104,71 @@ def walker_signals(k, T, nt, chol):
     return sig
 
 
+def nchunks(m, d):
+    return (m - 1) // d if m >= 1 else 0
+
+
+def key(t, T, d):
+    """(deadline, ready step, TRSM before GEMM): the queue order of build_tasks."""
+    kind, j, k0, q, r0, r1 = decode(t)
+    if kind != GEMM:
+        return (k0, k0, 0)
+    if q == 1:
+        dl = k0 + 1
+    else:
+        c = k0 // d
+        dls = []
+        for i in tiles(r0, r1, T):
+            nc = nchunks(min(i, j), d)
+            dls.append((c + 2) * d - 1 if c + 1 < nc else nc * d)
+        dl = min(dls)
+    return (dl, k0 + q - 1, 1)
+
+
 def interleaved(tasks, nt, T, chol, nurg, d):
-    """A sequential execution the kernel's queues admit: per step k the walker,
-    then the urgent tasks of ready step k, then the bulk tasks of ready step k,
-    each queue in its own order.  Every wait condition (and every operand of a
-    chunked GEMM) must hold when its task is reached; together with the
-    per-queue ready-step order this is the kernel's deadlock-freedom argument
-    (see build_tasks)."""
+    """A sequential execution the kernel's in-order queues admit: repeatedly run
+    the walker's next step, else the urgent queue's head, else the bulk queue's
+    head — whichever has every wait condition (and every operand of a chunked
+    GEMM) satisfied.  Getting stuck would mean the persistent kernel can
+    deadlock; each queue must also be sorted by the (deadline, ready step,
+    kind) key that makes the order topological (see build_tasks)."""
     urg, bulk = tasks[:nurg], tasks[nurg:]
     for q in (urg, bulk):
-        rs = [ready(t) for t in q]
-        assert all(x <= y for x, y in zip(rs, rs[1:])), "queue not in ready-step order"
+        ks = [key(t, T, d) for t in q]
+        assert all(x <= y for x, y in zip(ks, ks[1:])), "queue not in key order"
     cnt = np.zeros((nt, nt), dtype=np.int64)
     out = []
-    iu = ib = 0
-    for k in range(nt):
-        for tile, nd in walker_needs(k, T, nt, chol, d):
-            assert cnt[tile] >= nd, ("walker", k, tile, nd, cnt[tile])
-        out.append(("W", k))
-        for tile, rows in walker_signals(k, T, nt, chol).items():
-            cnt[tile] += rows
-        for q, idx in ((urg, "u"), (bulk, "b")):
-            i = iu if idx == "u" else ib
-            while i < len(q) and ready(q[i]) == k:
-                t = q[i]
-                kind, j, k0, qq, r0, r1 = decode(t)
-                for tile, nd in needs(kind, j, k0, qq, r0, r1, T, chol, d, full=True):
-                    assert cnt[tile] >= nd, (idx, t, tile, nd, cnt[tile])
-                out.append(("Q", t))
-                for tile, rows in signals(kind, j, k0, r0, r1, T).items():
-                    cnt[tile] += rows
-                i += 1
-            if idx == "u":
-                iu = i
+    iu = ib = wk = 0
+
+    def ok(need):
+        return all(cnt[tile] >= nd for tile, nd in need)
+
+    while wk < nt or iu < len(urg) or ib < len(bulk):
+        if wk < nt and ok(walker_needs(wk, T, nt, chol, d)):
+            out.append(("W", wk))
+            for tile, rows in walker_signals(wk, T, nt, chol).items():
+                cnt[tile] += rows
+            wk += 1
+            continue
+        ran = False
+        for qn in ("u", "b"):
+            q, i = (urg, iu) if qn == "u" else (bulk, ib)
+            if i >= len(q):
+                continue
+            t = q[i]
+            kind, j, k0, qq, r0, r1 = decode(t)
+            if not ok(needs(kind, j, k0, qq, r0, r1, T, chol, d, full=True)):
+                continue
+            out.append(("Q", t))
+            for tile, rows in signals(kind, j, k0, r0, r1, T).items():
+                cnt[tile] += rows
+            if qn == "u":
+                iu += 1
             else:
-                ib = i
-    assert iu == len(urg) and ib == len(bulk)
+                ib += 1
+            ran = True
+            break
+        assert ran, ("stuck", wk, iu, ib)
     return out
 
 

@@ -1,0 +1,65 @@
+#!/usr/bin/env python3
+"""T1 / T8 time-to-best on the virtual-clock harness.
+
+For each seed: a 1-evaluator and a W-evaluator BayesOpt run with the same kernel,
+inputs, seed and budget, every evaluation measured for real on one B200
+(tt_tune_virtual: W evaluators emulated on a virtual clock, the real host ask
+time charged serially).
+  T1 = elapsed_s at which the 1-evaluator run first reaches its final best;
+  TW = elapsed_s at which the W-evaluator run first records a runtime <= that best
+       or evaluates the same configuration.
+Prints one JSON line per seed and a summary (median ratio over seeds).
+
+    python tools/t1t8.py --kernel 3mm --size extralarge --evals 200 --workers 8 --seeds 1,2,3
+"""
+import argparse
+import json
+import statistics
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2309_07235_b200 import tuning  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--kernel", default="3mm")
+ap.add_argument("--size", default="extralarge")
+ap.add_argument("--evals", type=int, default=200)
+ap.add_argument("--workers", type=int, default=8)
+ap.add_argument("--seeds", default="1,2,3")
+ap.add_argument("--out", default=None)
+a = ap.parse_args()
+FLOPS = {"3mm": 2.0 * (1600 * 1800 * 2000 + 2000 * 2200 * 2400 + 1600 * 2000 * 2400),
+         "cholesky": 4000 ** 3 / 3.0, "lu": 2.0 / 3.0 * 4000 ** 3}
+rows = []
+for seed in [int(s) for s in a.seeds.split(",")]:
+    t0 = time.time()
+    r1, tot1 = tuning.run_tuning_virtual("bayesopt", a.kernel, a.size, seed, a.evals, workers=1)
+    rw, totw = tuning.run_tuning_virtual("bayesopt", a.kernel, a.size, seed, a.evals,
+                                         workers=a.workers)
+    b1 = tuning.best_record(r1)
+    t1 = b1.elapsed_s
+    tw = tuning.time_to_reach(rw, b1.runtime_s, b1.flat)
+    bw = tuning.best_record(rw)
+    ok1 = [r for r in r1 if r.runtime_s is not None]
+    row = {"kernel": a.kernel, "size": a.size, "seed": seed, "evals": a.evals,
+           "workers": a.workers, "T1_s": t1, "TW_s": tw, "ratio": t1 / tw if tw > 0 else None,
+           "best1_cfg": list(b1.config), "best1_ms": b1.runtime_s * 1e3,
+           "bestW_cfg": list(bw.config), "bestW_ms": bw.runtime_s * 1e3,
+           "total1_s": tot1, "totalW_s": totw,
+           "mean_eval_s": statistics.mean(r.eval_s for r in r1),
+           "mean_ask_s_per_eval_1": statistics.mean(r.ask_s for r in r1),
+           "mean_ask_s_per_eval_W": statistics.mean(r.ask_s for r in rw),
+           "wall_s": time.time() - t0}
+    if a.kernel in FLOPS and a.size == "extralarge":
+        row["best1_pct_of_fp64_peak"] = 100 * FLOPS[a.kernel] / b1.runtime_s / 1e12 / 37.05
+        row["bestW_pct_of_fp64_peak"] = 100 * FLOPS[a.kernel] / bw.runtime_s / 1e12 / 37.05
+    rows.append(row)
+    print(json.dumps(row), flush=True)
+ratios = [r["ratio"] for r in rows if r["ratio"]]
+summary = {"summary": True, "median_ratio": statistics.median(ratios) if ratios else None,
+           "ratios": ratios, "median_best1_pct": statistics.median(r.get("best1_pct_of_fp64_peak", 0) for r in rows)}
+print(json.dumps(summary), flush=True)
+if a.out:
+    Path(a.out).write_text("\n".join(json.dumps(r) for r in rows + [summary]) + "\n")
