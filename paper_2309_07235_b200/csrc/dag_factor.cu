@@ -148,13 +148,13 @@ __device__ bool wait_ge(const Params& p, const int* addr, int need) {
 }
 
 // Counter targets (finished rows) under the chunked stage numbering
-// (dag_factor.cuh): a tile with m updates has finished the stages covering
-// the steps < s, resp. is final.
-__device__ __forceinline__ int need_before(const Params& p, int m, int s) {
-  return stages_before(m, s, p.d) * p.T;
+// (dag_factor.cuh): tile (i, col), m = min(i, col) updates, has finished the
+// stages covering the steps < s, resp. is final.
+__device__ __forceinline__ int need_before(const Params& p, int m, int col, int s) {
+  return stages_before(m, s, p.d, col % p.d) * p.T;
 }
-__device__ __forceinline__ int need_final(const Params& p, int m) {
-  return stages_total(m, p.d) * p.T;
+__device__ __forceinline__ int need_final(const Params& p, int m, int col) {
+  return stages_total(m, p.d, col % p.d) * p.T;
 }
 
 // Task-level dependencies: what the whole CTA reads (the diagonal tile, the
@@ -176,15 +176,15 @@ __device__ __forceinline__ void dep_at(const Params& p, int kind, int j, int k, 
   switch (kind) {
     case kTrsmL:  // DIAG(k)
       *idx = k * nt + k;
-      *need = need_final(p, k);
+      *need = need_final(p, k, k);
       return;
     case kTrsmU:  // every update of tile (k,j), DIAG(k)
       *idx = d == 0 ? k * nt + j : k * nt + k;
-      *need = d == 0 ? need_before(p, k, k) : need_final(p, k);
+      *need = d == 0 ? need_before(p, k, j, k) : need_final(p, k, k);
       return;
     default:  // kGemm over steps [k0, k]: B operand U(k, j) / L(j, k) final
       *idx = CHOL ? j * nt + k : k * nt + j;
-      *need = need_final(p, k);
+      *need = need_final(p, k, CHOL ? k : j);
   }
 }
 
@@ -221,7 +221,7 @@ __device__ __forceinline__ bool strip_deps(const Params& p, int rs, int re, int 
   if (d < (kl >= 0 ? 2 * nti : nti)) {
     const int i = ti0 + (d < nti ? d : d - nti);
     const int* c = &p.cnt[i * nt + (d < nti ? col : kl)];
-    const int need = d < nti ? need_before(p, min(i, col), s) : need_final(p, kl);
+    const int need = d < nti ? need_before(p, min(i, col), col, s) : need_final(p, kl, kl);
     if (block) {
       ok = wait_ge(p, c, need);
     } else {
@@ -1057,7 +1057,7 @@ __device__ void walker(const Params& p, double* dsm) {
     stamp(k, 0);
     // the updates of steps < k-1 of tile (k,k) come from the queue's GEMM
     // tasks (step k-1 is always a single step: the walker applies it)
-    if (k >= 2 && !wait1(&p.cnt[k * nt + k], need_before(p, k, k - 1))) return;
+    if (k >= 2 && !wait1(&p.cnt[k * nt + k], need_before(p, k, k, k - 1))) return;
     stamp(k, 1);
     tile_load<CHOL>(D, dk, ld, T);
     __syncthreads();
@@ -1110,8 +1110,8 @@ __device__ void walker(const Params& p, double* dsm) {
     if (!s_ok) return;
     if (k + 1 >= nt) break;
     // ---- first tiles of the panel: L(k+1,k) = A(k+1,k) U11^-1, U(k,k+1) = L11^-1 A(k,k+1)
-    if (!wait1(&p.cnt[(k + 1) * nt + k], need_before(p, k, k))) return;
-    if (!CHOL && !wait1(&p.cnt[k * nt + k + 1], need_before(p, k, k))) return;
+    if (!wait1(&p.cnt[(k + 1) * nt + k], need_before(p, k, k, k))) return;
+    if (!CHOL && !wait1(&p.cnt[k * nt + k + 1], need_before(p, k, k + 1, k))) return;
     stamp(k, 4);
     {
       const double* al = p.a + static_cast<long long>(kT + T) * ld + kT;
@@ -1612,17 +1612,32 @@ std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
   };
   std::vector<Keyed> urg, bulk;
   bulk.reserve(static_cast<size_t>(count_tasks(chol, n, by, bx)));
-  // is [k0, k0+q) one stage of tile (i, j)?
-  auto is_stage = [&](int i, int jj, int k0, int q) {
-    const int m = std::min(i, jj), nc = nchunks(m, d);
-    if (q == d && k0 % d == 0 && k0 + d <= nc * d) return true;  // a full chunk
-    return q == 1 && k0 >= nc * d && k0 < m;                      // a single step
+  // chunk of column jj (phase o = jj mod d) that closes at step r+1, if any:
+  // [k0, r+1) with q = r+1-k0
+  auto chunk_closing = [&](int jj, int r, int* k0) {
+    const int o = jj % d, b = r + 1;
+    if (d == 1) return false;
+    if (o > 0 && b == o) {
+      *k0 = 0;
+      return true;
+    }
+    if (b > o && b >= d && (b - o) % d == 0) {
+      *k0 = b - d;
+      return true;
+    }
+    return false;
+  };
+  // is [k0, k0+q) one stage of tile (i, j)?  (a chunk of column j ending at or
+  // before the tile's first single step, or a single step before m)
+  auto is_stage = [&](int i, int jj, int k0, int q, bool chunk) {
+    const int m = std::min(i, jj), e = chunk_end(m, d, jj % d);
+    return chunk ? k0 + q <= e : (q == 1 && k0 >= e && k0 < m);
   };
   // earliest ready step of the next stage of tile (i, j) after [k0, k0+q)
-  auto deadline = [&](int i, int jj, int k0, int q) {
-    if (q == 1) return k0 + 1;
-    const int nc = nchunks(std::min(i, jj), d), c = k0 / d;
-    return c + 1 < nc ? (c + 2) * d - 1 : nc * d;
+  auto deadline = [&](int i, int jj, int k0, int q, bool chunk) {
+    if (!chunk) return k0 + 1;
+    const int e = chunk_end(std::min(i, jj), d, jj % d), end = k0 + q;
+    return end < e ? end + d - 1 : e;  // the next chunk's ready step, or the first single
   };
   for (int r = 0; r + 1 < nt; ++r) {
     const int pe = (r + 1) * T;
@@ -1645,36 +1660,39 @@ std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
     for (const auto& rg : reg) task(kTrsmL, std::max(rg.first, pe + T), rg.second, 0, r, 1, r);  // row r+1: walker
     if (!chol)
       for (int j = r + 2; j < nt; ++j) task(kTrsmU, 0, 1, j, r, 1, r);
-    // GEMM intervals ready at step r: the single step r, then the chunk
-    // [r+1-d, r+1) when r+1 closes one
-    std::vector<std::pair<int, int>> ivals{{r, 1}};
-    if (d > 1 && (r + 1) % d == 0) ivals.emplace_back(r + 1 - d, d);
+    // GEMMs ready at step r, per tile column: the single step r, and the
+    // column's chunk closing at r+1 (if its phase puts a boundary there)
     const int ncols = nt - r - 1, nreg = static_cast<int>(reg.size());
     const bool merge = gm.rows > 0 && static_cast<long long>(nreg) * ncols >= gm.thresh;
-    for (const auto& iv : ivals) {
-      const int k0 = iv.first, q = iv.second;
-      // row regions outer: a region's GEMMs need only that region's L21 rows
-      // (plus the U12 tiles), so the first GEMMs taken are the first ready.
-      // Steps with many GEMM tasks may group consecutive regions into one
-      // task (TT_DAG_MERGE; off by default).
+    // row regions outer: a region's GEMMs need only that region's L21 rows
+    // (plus the U12 tiles), so the first GEMMs taken are the first ready.
+    // Steps with many GEMM tasks may group consecutive regions into one
+    // single-step task (TT_DAG_MERGE; off by default).
+    for (int pass = 0; pass < 2; ++pass) {  // singles, then chunks
+      const bool chunk = pass == 1;
       for (int g0 = 0, g1; g0 < nreg; g0 = g1) {
         g1 = g0 + 1;  // regions [g0, g1) form one task: at least gm.rows rows when merging
-        while (merge && q == 1 && g1 < nreg && reg[g1 - 1].second - reg[g0].first < gm.rows) ++g1;
+        while (merge && !chunk && g1 < nreg && reg[g1 - 1].second - reg[g0].first < gm.rows) ++g1;
         const int lo = reg[g0].first, hi = reg[g1 - 1].second;
         for (int j = r + 1; j < nt; ++j) {
+          int k0 = r, q = 1;
+          if (chunk) {
+            if (!chunk_closing(j, r, &k0)) continue;
+            q = r + 1 - k0;
+          }
           int r0 = std::max(lo, chol ? j * T : pe);  // Cholesky: lower triangle only
-          if (q == 1 && j == r + 1) r0 = std::max(r0, pe + T);  // tile (r+1,r+1): the walker
+          if (!chunk && j == r + 1) r0 = std::max(r0, pe + T);  // tile (r+1,r+1): the walker
           // maximal runs of tiles for which [k0, k0+q) is a stage
           for (int x = r0; x < hi;) {
             const int i = x / T;
             const int xe = std::min(hi, (i + 1) * T);
-            if (!is_stage(i, j, k0, q)) {
+            if (!is_stage(i, j, k0, q, chunk)) {
               x = xe;
               continue;
             }
-            int y = xe, dl = deadline(i, j, k0, q);
-            while (y < hi && is_stage(y / T, j, k0, q)) {
-              dl = std::min(dl, deadline(y / T, j, k0, q));
+            int y = xe, dl = deadline(i, j, k0, q, chunk);
+            while (y < hi && is_stage(y / T, j, k0, q, chunk)) {
+              dl = std::min(dl, deadline(y / T, j, k0, q, chunk));
               y = std::min(hi, (y / T + 1) * T);
             }
             task(kGemm, x, y, j, k0, q, dl);

@@ -31,24 +31,43 @@ enum TaskKind : int { kDiag = 0, kTrsmL = 1, kTrsmU = 2, kGemm = 3 };
 // Chunked trailing updates.  A GEMM task applies the updates of q
 // consecutive panel steps [k0, k0+q) to its rows at once (C stays in
 // registers; K = q*bx), so the C round trip, the task's dependency waits and
-// its operand staging are paid once per q steps.  The steps of tile (i, j),
-// m = min(i, j) of them before its own DIAG/TRSM, are applied in
-//   nchunks(m) full chunks of d steps [c*d, (c+1)*d)   (bulk tiles), then
-//   single steps [nchunks(m)*d, m)                      (1..d of them),
+// its operand staging are paid once per q steps.  Tile column j groups its
+// steps into chunks ending at the boundaries o, o+d, o+2d, ... with phase
+// o = j mod d (the first chunk [0, o) may be short): the columns' chunks
+// close on different steps, so the bulk work arrives evenly instead of in a
+// burst every d steps.  Tile (i, j), with m = min(i, j) updates before its own
+// DIAG/TRSM, gets
+//   the chunks of column j that end at or before step m-1,
+//   then single steps up to m-1,
 // so the last update of every tile — the one the diagonal chain waits for —
 // is always a single step.  Each chunk / single / the final op is one
 // "stage"; the tile counter counts finished rows over stages.  Per element
 // the products are accumulated in ascending step order in both cases: the
 // result is bitwise that of step-by-step updates (same DMMA sequence).
-__host__ __device__ inline int nchunks(int m, int d) { return m >= 1 ? (m - 1) / d : 0; }
+// Number of chunks of a tile with m updates in a column of phase o.
+__host__ __device__ inline int nchunks(int m, int d, int o) {
+  if (m < 1 || d <= 1) return 0;  // d = 1: every update a single step
+  if (o == 0) return (m - 1) / d;
+  return o <= m - 1 ? 1 + (m - 1 - o) / d : 0;
+}
+// End (exclusive) of the last chunk: the first single step.
+__host__ __device__ inline int chunk_end(int m, int d, int o) {
+  const int nc = nchunks(m, d, o);
+  if (o == 0) return nc * d;
+  return nc == 0 ? 0 : o + (nc - 1) * d;
+}
 // Stages of a tile with m updates that cover the steps < s (s a chunk
 // boundary or a single step of that tile, s <= m).
-__host__ __device__ inline int stages_before(int m, int s, int d) {
-  const int nc = nchunks(m, d);
-  return s <= nc * d ? s / d : nc + (s - nc * d);
+__host__ __device__ inline int stages_before(int m, int s, int d, int o) {
+  const int e = chunk_end(m, d, o);
+  if (s > e) return nchunks(m, d, o) + (s - e);
+  if (s == 0) return 0;
+  return o == 0 ? s / d : 1 + (s - o) / d;
 }
 // Stages of a tile with m updates, its final DIAG/TRSM included.
-__host__ __device__ inline int stages_total(int m, int d) { return stages_before(m, m, d) + 1; }
+__host__ __device__ inline int stages_total(int m, int d, int o) {
+  return stages_before(m, m, d, o) + 1;
+}
 
 // Widest tile the persistent kernel handles (the diag block is factored by
 // the warp-register code of diag_factor.cuh, <= 64).

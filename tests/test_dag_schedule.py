@@ -39,15 +39,36 @@ def tiles(r0, r1, T):
     return range(r0 // T, (r1 - 1) // T + 1)
 
 
-def stages_before(m, s, d):
-    """dag_factor.cuh: stages of a tile with m updates covering the steps < s
-    (nchunks(m) full chunks of d steps, then single steps)."""
-    nc = (m - 1) // d if m >= 1 else 0
-    return s // d if s <= nc * d else nc + (s - nc * d)
+def nchunks(m, d, o):
+    """dag_factor.cuh: chunks of a tile with m updates in a column of phase o
+    (boundaries o, o+d, o+2d, ... ending at or before step m-1)."""
+    if m < 1 or d <= 1:
+        return 0
+    if o == 0:
+        return (m - 1) // d
+    return 1 + (m - 1 - o) // d if o <= m - 1 else 0
 
 
-def fin(m, d):
-    return stages_before(m, m, d) + 1
+def chunk_end(m, d, o):
+    nc = nchunks(m, d, o)
+    if o == 0:
+        return nc * d
+    return 0 if nc == 0 else o + (nc - 1) * d
+
+
+def stages_before(m, s, d, col):
+    """Stages of tile column `col` (phase col % d) with m updates covering steps < s."""
+    o = col % d
+    e = chunk_end(m, d, o)
+    if s > e:
+        return nchunks(m, d, o) + (s - e)
+    if s == 0:
+        return 0
+    return s // d if o == 0 else 1 + (s - o) // d
+
+
+def fin(m, d, col):
+    return stages_before(m, m, d, col) + 1
 
 
 def ready(t):
@@ -60,19 +81,19 @@ def needs(kind, j, k0, q, r0, r1, T, chol, d, full=False):
     only for the operands of step kl; full=True lists every step's operands,
     which the chain argument (dag_factor.cu, dep_at) says are then final too."""
     if kind == DIAG:
-        return [((k0, k0), stages_before(k0, k0 - 1, d) * T)]
+        return [((k0, k0), stages_before(k0, k0 - 1, d, k0) * T)]
     if kind == TRSM_L:
-        return [((i, k0), stages_before(k0, k0, d) * T) for i in tiles(r0, r1, T)] + \
-            [((k0, k0), fin(k0, d) * T)]
+        return [((i, k0), stages_before(k0, k0, d, k0) * T) for i in tiles(r0, r1, T)] + \
+            [((k0, k0), fin(k0, d, k0) * T)]
     if kind == TRSM_U:
-        return [((k0, j), stages_before(k0, k0, d) * T), ((k0, k0), fin(k0, d) * T)]
+        return [((k0, j), stages_before(k0, k0, d, j) * T), ((k0, k0), fin(k0, d, k0) * T)]
     kl = k0 + q - 1
     ks = range(k0, kl + 1) if full else [kl]
     out = []
     for i in tiles(r0, r1, T):
-        out.append(((i, j), stages_before(min(i, j), k0, d) * T))
-        out += [((i, k), fin(k, d) * T) for k in ks]
-    return out + [(((j, k) if chol else (k, j)), fin(k, d) * T) for k in ks]
+        out.append(((i, j), stages_before(min(i, j), k0, d, j) * T))
+        out += [((i, k), fin(k, d, k) * T) for k in ks]
+    return out + [(((j, k) if chol else (k, j)), fin(k, d, k if chol else j) * T) for k in ks]
 
 
 def signals(kind, j, k0, r0, r1, T):
@@ -87,11 +108,11 @@ def signals(kind, j, k0, r0, r1, T):
 def walker_needs(k, T, nt, chol, d):
     out = []
     if k >= 1:
-        out.append(((k, k), stages_before(k, k - 1, d) * T))
+        out.append(((k, k), stages_before(k, k - 1, d, k) * T))
     if k + 1 < nt:
-        out.append(((k + 1, k), stages_before(k, k, d) * T))
+        out.append(((k + 1, k), stages_before(k, k, d, k) * T))
         if not chol:
-            out.append(((k, k + 1), stages_before(k, k, d) * T))
+            out.append(((k, k + 1), stages_before(k, k, d, k + 1) * T))
     return out
 
 
@@ -104,25 +125,19 @@ def walker_signals(k, T, nt, chol):
     return sig
 
 
-def nchunks(m, d):
-    return (m - 1) // d if m >= 1 else 0
-
-
 def key(t, T, d):
     """(deadline, ready step, TRSM before GEMM): the queue order of build_tasks."""
     kind, j, k0, q, r0, r1 = decode(t)
     if kind != GEMM:
         return (k0, k0, 0)
-    if q == 1:
-        dl = k0 + 1
-    else:
-        c = k0 // d
-        dls = []
-        for i in tiles(r0, r1, T):
-            nc = nchunks(min(i, j), d)
-            dls.append((c + 2) * d - 1 if c + 1 < nc else nc * d)
-        dl = min(dls)
-    return (dl, k0 + q - 1, 1)
+    dls = []
+    for i in tiles(r0, r1, T):
+        e = chunk_end(min(i, j), d, j % d)
+        if k0 + q <= e:  # a chunk: the next chunk's ready step, or the first single
+            dls.append(k0 + q + d - 1 if k0 + q < e else e)
+        else:
+            dls.append(k0 + 1)
+    return (min(dls), k0 + q - 1, 1)
 
 
 def interleaved(tasks, nt, T, chol, nurg, d):
@@ -195,13 +210,13 @@ def test_task_order_and_coverage(kernel, n, by, bx):
             if chol:
                 assert i >= jj, t
             cnt[tile] += rows
-            assert cnt[tile] <= fin(min(i, jj), d) * T, (what, t, tile)
+            assert cnt[tile] <= fin(min(i, jj), d, jj) * T, (what, t, tile)
     for i in range(nt):
         for jj in range(nt):
             if chol and jj > i:
                 assert cnt[i, jj] == 0
             else:
-                assert cnt[i, jj] == fin(min(i, jj), d) * T, (i, jj)
+                assert cnt[i, jj] == fin(min(i, jj), d, jj) * T, (i, jj)
 
 
 def test_chunked_updates_present():
@@ -212,7 +227,7 @@ def test_chunked_updates_present():
         assert d >= 4
         qs = tasks[:, 1] >> 16
         gem = (tasks[:, 0] & 3) == GEMM
-        assert np.any(qs[gem] == d) and np.all((qs[gem] == 1) | (qs[gem] == d))
+        assert np.any(qs[gem] == d) and np.all(qs[gem] <= d)
 
 
 def run_tasks_numpy(a, tasks, bx, chol, nurg, d):
