@@ -431,9 +431,11 @@ def schedule_info(lib, kid, n, by, bx):
     ntasks = lib.tt_dag_tasks(kid, n, by, bx, None, 0)
     if ntasks < 0:
         return {"kind": "graph", "kernel": "panel/trsm/dgemm graph (schedules.cu)"}
-    return {"kind": "persistent tile-DAG", "kernel": f"dag_kernel<{(bx + 7) // 8}, {'CHOL' if kid else 'LU'}>",
+    t = lib.tt_dag_tile(n, by, bx)
+    return {"kind": "persistent tile-DAG", "kernel": f"dag_kernel<{(t + 7) // 8}, {'CHOL' if kid else 'LU'}>",
+            "tile": t, "region_rows": lib.tt_dag_region_rows(n, by, bx),
             "queue_tasks": ntasks, "urgent_tasks": lib.tt_dag_urgent(kid, n, by, bx),
-            "walker_steps": n // bx, "chunk_depth": lib.tt_dag_chunk_depth(n, by, bx)}
+            "walker_steps": n // t, "chunk_depth": lib.tt_dag_chunk_depth(n, by, bx)}
 
 
 EXTRA_CASES = [

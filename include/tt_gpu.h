@@ -156,9 +156,19 @@ int tt_dev_fill_uniform(tt_ctx* ctx, double* a, int rows, int cols, int ld, long
  * runs on the launch-per-kernel graph schedule instead.  Needs no device. */
 int tt_dag_tasks(int kernel, int n, int by, int bx, int* out, int cap);
 /* Chunk depth d of that schedule: bulk tiles receive their updates d steps
- * at a time (K = d * bx), the last 1..d steps of each tile singly; -1 when
- * the graph schedule runs. */
+ * at a time (K = d * T, T = tt_dag_tile), the last 1..d steps of each tile
+ * singly; -1 when the graph schedule runs. */
 int tt_dag_chunk_depth(int n, int by, int bx);
+/* Tile T of that schedule for panel width bx: bx itself for 8 <= bx <= 64,
+ * the largest divisor of bx in [8, 64] for wider panels (whose bulk tiles
+ * take bx/T steps per update, the reference's rank-bx trailing update), the
+ * smallest multiple of bx in [8, 64] dividing n for bx < 8; -1 when the
+ * graph schedule runs. */
+int tt_dag_tile(int n, int by, int bx);
+/* Row extent of that schedule's update / solve tasks: by packed to at least
+ * max(128, 5120 / T) rows (adjacent by-row regions per task); -1 when the
+ * graph schedule runs. */
+int tt_dag_region_rows(int n, int by, int bx);
 /* Number of leading tasks of that list forming the urgent queue (the rest is
  * the bulk queue); -1 when the graph schedule runs instead. */
 int tt_dag_urgent(int kernel, int n, int by, int bx);

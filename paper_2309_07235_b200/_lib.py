@@ -26,7 +26,8 @@ EXPORTS = (
     "tt_setup_host", "tt_setup_seeded", "tt_run", "tt_measure", "tt_measure_samples",
     "tt_get_input", "tt_residual", "tt_dev_lu", "tt_dev_cholesky", "tt_dev_mm3",
     "tt_dev_gemm", "tt_dev_fill_uniform", "tt_launch_count", "tt_build_info", "tt_dag_tasks",
-    "tt_dag_trace", "tt_dag_urgent", "tt_dag_chunk_depth", "tt_lu_factor_batch", "tt_cholesky_factor_batch",
+    "tt_dag_trace", "tt_dag_urgent", "tt_dag_chunk_depth", "tt_dag_tile", "tt_dag_region_rows",
+    "tt_lu_factor_batch", "tt_cholesky_factor_batch",
 )
 
 _lib = None
@@ -74,6 +75,8 @@ def load() -> ctypes.CDLL:
         "tt_dag_trace": (c_int, [vp, vp, c_int]),
         "tt_dag_urgent": (c_int, [c_int, c_int, c_int, c_int]),
         "tt_dag_chunk_depth": (c_int, [c_int, c_int, c_int]),
+        "tt_dag_tile": (c_int, [c_int, c_int, c_int]),
+        "tt_dag_region_rows": (c_int, [c_int, c_int, c_int]),
         "tt_lu_factor_batch": (c_int, [vp, vp, c_int, c_int, c_int, c_int, c_int_p]),
         "tt_cholesky_factor_batch": (c_int, [vp, vp, c_int, c_int, c_int, c_int, c_int_p]),
     }
@@ -111,6 +114,18 @@ def dag_tasks(kernel: str, n: int, by: int, bx: int) -> np.ndarray | None:
     out = np.zeros((cnt, 4), dtype=np.int32)
     lib.tt_dag_tasks(kid, n, by, bx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), cnt)
     return out
+
+
+def dag_tile(n: int, by: int, bx: int) -> int | None:
+    """Tile T the persistent schedule runs for (n, by, bx), None on the graph schedule."""
+    t = load().tt_dag_tile(n, by, bx)
+    return None if t < 0 else int(t)
+
+
+def dag_region_rows(n: int, by: int, bx: int) -> int | None:
+    """Row extent of the persistent schedule's update / solve tasks (by packed to >= 128)."""
+    r = load().tt_dag_region_rows(n, by, bx)
+    return None if r < 0 else int(r)
 
 
 def dag_chunk_depth(n: int, by: int, bx: int) -> int | None:

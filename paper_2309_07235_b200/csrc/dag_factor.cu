@@ -95,6 +95,10 @@ struct Params {
   int nuw;        // CTAs 1..nuw serve the urgent queue
   int d;          // chunk depth (dag_factor.cuh)
   int eager_sig;  // publish GEMM strips right after their stores: 0 no, 1 all, 2 urgent, 3 bulk
+  int fence;      // TT_DAG_FENCE=1: gpu-scope fence after each task's dependency wait
+  int pipe;       // GEMM tasks through gemm_pipe (TT_DAG_PIPE=0: the register path)
+  int nodeps;     // TT_DAG_NODEPS=1 (measurement aid): every counter starts satisfied and
+                  // no walker runs — the queues' task throughput alone, numerics void
   int pf_mask;    // bit 0: urgent CTAs, bit 1: bulk CTAs fetch the next task before
                   // the current one's dependency wait (else when warp 0 finishes it)
 };
@@ -137,6 +141,14 @@ __device__ bool wait_ge(const Params& p, const int* addr, int need) {
       if ((it & 15) == 15) {
         if (ld_relaxed(p.abort)) return false;
         if (globaltimer() - t0 > static_cast<unsigned long long>(kWatchdogNs)) {
+          // first expiring waiter records what it waited for (diagnostics:
+          // CTA, counter index, target, last value seen)
+          if (atomicCAS(p.abort + 2, 0, 1) == 0) {
+            p.abort[3] = blockIdx.x;
+            p.abort[4] = static_cast<int>(addr - p.cnt);
+            p.abort[5] = need;
+            p.abort[6] = ld_relaxed(addr);
+          }
           atomicExch(p.abort, 2);
           atomicMin(p.info, kTimeout);
           return false;
@@ -559,12 +571,13 @@ __device__ void gemm_task(const Params& p, int j, int k0, int q, int r0, int r1,
             for (int nf = 0; nf < NF; ++nf)
               bv[nf] = *reinterpret_cast<const double2*>(B + (8 * nf + g) * NPB + 8 * s + 2 * t);
 #pragma unroll
-            for (int mf = 0; mf < kMF; ++mf)
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-              for (int nf = 0; nf < NF; ++nf) {
-                dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a[mf][s].x, bv[nf].x);
-                dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a[mf][s].y, bv[nf].y);
-              }
+              for (int mf = 0; mf < kMF; ++mf)
+#pragma unroll
+                for (int nf = 0; nf < NF; ++nf)
+                  dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], h ? a[mf][s].y : a[mf][s].x,
+                             h ? bv[nf].y : bv[nf].x);
           } else {  // Bs[k][n]
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -622,6 +635,254 @@ __device__ void gemm_task(const Params& p, int j, int k0, int q, int r0, int r1,
     } else {
       prev_ra = ra;
       prev_nr = nr;
+    }
+  }
+  if (prev_ra >= 0) warp_signal(p, prev_ra, prev_ra + prev_nr, j);
+}
+
+// ---- pipelined strip GEMM (every GEMM task, q >= 1):
+// C(rows, j) -= sum_{k in [k0, k0+q)} L(rows, k) * B_k.
+//
+// Each warp walks its 16-row strips (ra = r0 + 16 warp + 128 i) as a stream
+// of items — per strip the q A-step operands L(strip, k0+kk) and then the
+// strip's C tile — copied by cp.async.cg (L2 only) into a per-warp ring of
+// R shared-memory slots, up to R-1 items ahead of the one being consumed:
+// the next steps' and the next strip's operands are in flight while the
+// current step's DMMAs run, so no L2 round trip sits between two steps or two
+// strips (the register path above paid one per strip).  The accumulators
+// start from zero and C is read last: C - sum A_k B_k, so the C tile's own
+// dependency (its earlier stages) is only waited for when its item is issued.
+// An item whose inputs are not yet published is issued when it is next to be
+// consumed (blocking there only); items are issued in order, so the cp.async
+// groups retire in order.  The B tiles (q stacked, stage_b) are staged once
+// per task, their copies in flight together with each warp's first items.
+__host__ __device__ constexpr int sa_stride(int tp) { return tp % 16 == 8 ? tp : tp + 8; }
+__host__ __device__ constexpr int ring_slots(int nf) { return nf <= 5 ? 3 : 2; }
+__host__ __device__ constexpr int ring_doubles(int nf) {
+  return kWarps * ring_slots(nf) * kStrip * sa_stride(nf * 8);
+}
+// B tiles first (q stacked), the rings after them (16-byte aligned)
+__host__ __device__ constexpr int ring_offset(int q, int tp, bool chol) {
+  return (q * tp * bstride(tp, chol) + 1) & ~1;
+}
+
+__device__ __forceinline__ void cp_async_wait_n(int n) {
+  switch (n) {
+    case 0: cp_async_wait<0>(); break;
+    case 1: cp_async_wait<1>(); break;
+    case 2: cp_async_wait<2>(); break;
+    default: cp_async_wait<3>(); break;
+  }
+}
+
+// Rows [rs, re) of tile column kl final (the L rows a GEMM over steps up to kl
+// reads); one poll per lane, `block` waits.
+__device__ __forceinline__ bool a_deps(const Params& p, int rs, int re, int kl, bool block) {
+  const int T = p.T, nt = p.nt;
+  const int ti0 = rs / T, nti = (re - 1) / T - ti0 + 1;
+  const int d = threadIdx.x & 31;
+  bool ok = true;
+  if (d < nti) {
+    const int* c = &p.cnt[(ti0 + d) * nt + kl];
+    const int need = need_final(p, kl, kl);
+    ok = block ? wait_ge(p, c, need) : ld_acquire(c) >= need;
+  }
+  return __all_sync(0xffffffffu, ok);
+}
+
+// Issues the cp.async copies of the B tiles (no wait: the caller's first
+// pipeline items join them in flight; gemm_pipe waits before its barrier).
+template <int NF, bool CHOL>
+__device__ __forceinline__ void stage_b_async(const Params& p, double* Bs, int j, int k0, int q) {
+  constexpr int Tp = NF * 8, NPB = bstride(Tp, CHOL), HP = Tp / 2;
+  const int T = p.T;
+  const long long ld = p.ld;
+  const int total = q * Tp * HP;  // element pairs
+  for (int e = threadIdx.x; e < total; e += kThreads) {
+    const int kk = e / (Tp * HP), rem = e - kk * (Tp * HP), x = rem / HP, y = 2 * (rem - x * HP);
+    const int k = k0 + kk;
+    const long long row = CHOL ? static_cast<long long>(j) * T + x : static_cast<long long>(k) * T + x;
+    const long long col = CHOL ? static_cast<long long>(k) * T + y : static_cast<long long>(j) * T + y;
+    const double* src = p.a + row * ld + col;
+    double* dst = Bs + kk * Tp * NPB + x * NPB + y;
+    if (!(T & 1)) {
+      const bool valid = x < T && y < T;
+      cp_async16_zfill(dst, valid ? src : p.a, valid);
+    } else {  // odd T: rows are not 16-byte aligned
+      dst[0] = (x < T && y < T) ? __ldcg(src) : 0.0;
+      dst[1] = (x < T && y + 1 < T) ? __ldcg(src + 1) : 0.0;
+    }
+  }
+  cp_async_commit();
+}
+
+template <int NF, bool CHOL>
+__device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
+                          double* __restrict__ smem, bool eager, unsigned long long* first_done) {
+  constexpr int Tp = NF * 8, NPB = bstride(Tp, CHOL), SA = sa_stride(Tp), R = ring_slots(NF);
+  constexpr int HP = Tp / 2, kSlot = kStrip * SA;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
+  const int T = p.T;
+  const long long ld = p.ld;
+  const int kl = k0 + q - 1, jT = j * T;
+  const bool vec = !(T & 1);  // rows and tile origins 16-byte aligned (ld even, base aligned)
+  const double* __restrict__ Bs = smem;
+  double* ring = smem + ring_offset(q, Tp, CHOL) + warp * R * kSlot;
+  const int first = r0 + warp * kStrip, stride = kWarps * kStrip;
+  const int ns = first < r1 ? (r1 - first + stride - 1) / stride : 0;
+  const int per = q + 1;  // items per strip: q A steps, then C
+  const int total = ns * per;
+  int issued = 0;
+
+  int is_i = 0, is_kk = 0;  // strip / item of the next item to issue
+  auto issue = [&](int y) {
+    const int i = is_i, kk = is_kk;
+    const int ra = first + i * stride, nr = min(kStrip, r1 - ra);
+    const double* src = p.a + static_cast<long long>(ra) * ld +
+                        (kk < q ? static_cast<long long>(k0 + kk) * T : static_cast<long long>(jT));
+    double* dst = ring + (y % R) * kSlot;
+    if (vec) {
+#pragma unroll 4
+      for (int e = lane; e < kStrip * HP; e += 32) {
+        const int r = e / HP, c = 2 * (e - r * HP);
+        const bool valid = r < nr && c < T;
+        cp_async16_zfill(dst + r * SA + c, valid ? src + static_cast<long long>(r) * ld + c : p.a, valid);
+      }
+    } else {  // odd T: synchronous copies (visible after the consumer's __syncwarp)
+      for (int e = lane; e < kStrip * Tp; e += 32) {
+        const int r = e / Tp, c = e - r * Tp;
+        dst[r * SA + c] = (r < nr && c < T) ? __ldcg(src + static_cast<long long>(r) * ld + c) : 0.0;
+      }
+    }
+    cp_async_commit();
+  };
+  // issue items up to x + R - 1 in order; item x itself waits for its inputs
+  // when `block_x` (false: only on abort)
+  auto pump = [&](int x, bool block_x) -> bool {
+    while (issued < total && issued < x + R) {
+      const int y = issued, i = is_i, kk = is_kk;
+      if (kk == 0 || kk == q) {
+        const int rs = first + i * stride, re = min(r1, rs + kStrip);
+        const bool blk = block_x && y == x;
+        const bool ok = kk == 0 ? a_deps(p, rs, re, kl, blk) : strip_deps(p, rs, re, j, k0, -1, blk);
+        if (!ok) {
+          if (blk) return false;  // aborted
+          break;
+        }
+      }
+      issue(y);
+      ++issued;
+      if (++is_kk == per) {
+        is_kk = 0;
+        ++is_i;
+      }
+    }
+    return true;
+  };
+
+  pump(0, false);  // first items in flight with the B tiles
+  cp_async_wait_n(issued);  // the oldest group: B
+  __syncthreads();
+  if (first_done && lane == 0) first_done[2] = globaltimer();
+
+  double acc[kMF][NF][2];
+#pragma unroll
+  for (int mf = 0; mf < kMF; ++mf)
+#pragma unroll
+    for (int nf = 0; nf < NF; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
+  int prev_ra = -1, prev_nr = 0;
+  for (int x = 0, i = 0, kk = 0; x < total; ++x) {
+    if (!pump(x, true)) return;
+    cp_async_wait_n(issued - x - 1);
+    __syncwarp();
+    const double* slot = ring + (x % R) * kSlot;
+    const int ra = first + i * stride, nr = min(kStrip, r1 - ra);
+    if (kk < q) {
+      if (first_done && lane == 0 && x == 0) first_done[1] = globaltimer();
+      const double* B = Bs + kk * Tp * NPB;
+#pragma unroll
+      for (int s = 0; s < NF; ++s) {
+        if (8 * s < T) {
+          double2 af[kMF];
+#pragma unroll
+          for (int mf = 0; mf < kMF; ++mf)
+            af[mf] = *reinterpret_cast<const double2*>(slot + (mf * 8 + g) * SA + 8 * s + 2 * t);
+          if (CHOL) {  // Bs[n][k]: both k-halves of lane t with one 16-byte load
+            double2 bv[NF];
+#pragma unroll
+            for (int nf = 0; nf < NF; ++nf)
+              bv[nf] = *reinterpret_cast<const double2*>(B + (8 * nf + g) * NPB + 8 * s + 2 * t);
+            // k-half outer: consecutive DMMAs on one accumulator are kMF*NF
+            // apart (back to back, the compiler pads the DMMA latency with NOPs)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int mf = 0; mf < kMF; ++mf)
+#pragma unroll
+                for (int nf = 0; nf < NF; ++nf)
+                  dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], h ? af[mf].y : af[mf].x,
+                             h ? bv[nf].y : bv[nf].x);
+          } else {  // Bs[k][n]
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              double bv[NF];
+#pragma unroll
+              for (int nf = 0; nf < NF; ++nf) bv[nf] = B[(8 * s + 2 * t + h) * NPB + 8 * nf + g];
+#pragma unroll
+              for (int mf = 0; mf < kMF; ++mf)
+#pragma unroll
+                for (int nf = 0; nf < NF; ++nf)
+                  dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], h ? af[mf].y : af[mf].x, bv[nf]);
+            }
+          }
+        }
+      }
+      // publish the previous strip once this one's first DMMAs are issued
+      if (kk == 0 && prev_ra >= 0) {
+        warp_signal(p, prev_ra, prev_ra + prev_nr, j);
+        prev_ra = -1;
+      }
+    } else {  // C item: C - sum, stores (Cholesky diagonal tiles: row >= col only)
+      const int lower_off = CHOL ? ra - jT : kNoLower;
+#pragma unroll
+      for (int mf = 0; mf < kMF; ++mf) {
+        const int r = mf * 8 + g;
+        if (r < nr) {
+          double* crow = p.a + static_cast<long long>(ra + r) * ld + jT;
+#pragma unroll
+          for (int nf = 0; nf < NF; ++nf) {
+            const int c = nf * 8 + 2 * t;
+            const double2 cv = *reinterpret_cast<const double2*>(slot + r * SA + c);
+            const double v0 = cv.x - acc[mf][nf][0], v1 = cv.y - acc[mf][nf][1];
+            const bool ok0 = c < T && r + lower_off >= c, ok1 = c + 1 < T && r + lower_off >= c + 1;
+            if (vec && ok0 && ok1) {
+              *reinterpret_cast<double2*>(crow + c) = make_double2(v0, v1);
+            } else {
+              if (ok0) crow[c] = v0;
+              if (ok1) crow[c + 1] = v1;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int mf = 0; mf < kMF; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
+      if (first_done && lane == 0) {
+        first_done[0] = globaltimer();
+        first_done = nullptr;
+      }
+      if (eager) {
+        warp_signal(p, ra, ra + nr, j);
+      } else {
+        prev_ra = ra;
+        prev_nr = nr;
+      }
+    }
+    __syncwarp();  // every lane's reads of this slot done before it is refilled
+    if (++kk == per) {
+      kk = 0;
+      ++i;
     }
   }
   if (prev_ra >= 0) warp_signal(p, prev_ra, prev_ra + prev_nr, j);
@@ -1231,7 +1492,7 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
   const int4 kNone = make_int4(-1, 0, 0, 0);
 
   if (blockIdx.x == 0) {
-    walker<NF, CHOL>(p, dsm);
+    if (!p.nodeps) walker<NF, CHOL>(p, dsm);
     return;
   }
   // queue of this CTA: [qlo, qhi) of the task array, its own counter
@@ -1259,8 +1520,12 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
         if (early && tk.x >= 0) nid = qlo + atomicAdd(qnext, 1);
       }
       const bool ok = tk.x >= 0 && wait_deps<CHOL>(p, tk);
+      // the polling lanes' acquires reach the other threads through the warp
+      // and CTA barriers (both morally strong: causality order is transitive),
+      // so no gpu-scope fence here (TT_DAG_FENCE=1 restores one)
+      __syncwarp();
       if (lane == 0) {
-        __threadfence();
+        if (p.fence) __threadfence();
         s_go = ok;
         if (early) {
           s_id[cur ^ 1] = nid;
@@ -1279,7 +1544,15 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
     stamp(1);
     stamp(2);
     stamp(3);
-    if (kind == kGemm && task_q(tk) > 1) {  // chunked: q steps, K = q*T
+    if (kind == kGemm && p.pipe) {  // pipelined strips, any q
+      stage_b_async<NF, CHOL>(p, sm, j, k, task_q(tk));
+      stamp(0);
+      // p.eager_sig: 0 none, 1 all GEMM tasks, 2 urgent-queue CTAs only, 3 bulk only
+      const bool eager =
+          p.eager_sig == 1 || (p.eager_sig == 2 && urgent_q) || (p.eager_sig == 3 && !urgent_q);
+      gemm_pipe<NF, CHOL>(p, j, k, task_q(tk), r0, r1, sm, eager,
+                          (p.trace && warp == 0) ? &s_ph[1] : nullptr);
+    } else if (kind == kGemm && task_q(tk) > 1) {  // chunked: q steps, K = q*T
       const int q = task_q(tk);
       stage_b<NF, CHOL>(p, sm, j, k, q);
       __syncthreads();
@@ -1487,6 +1760,9 @@ cudaError_t optin_all() {
 }
 
 long long count_tasks(bool chol, int n, int by, int bx) {
+  bx = tile_for(n, bx);
+  if (bx == 0) return kMaxTasks + 1;
+  by = region_rows(by, bx);
   const int nt = n / bx;
   long long total = 0;
   for (int k = 0; k + 1 < nt; ++k) {
@@ -1506,8 +1782,45 @@ cudaError_t configure_device() {
   return e != cudaSuccess ? e : optin_all<true>();
 }
 
+// Knob -> persistent schedule.  The reference's panel width
+// bx (kernels.cpp:181-182) is the rank of the bulk trailing update; the
+// diagonal chain is blocked at T <= 64 (what the walker's shared-memory tiles
+// hold), like LAPACK factoring an nb-wide panel with an inner blocking:
+//   8 <= bx <= 64: T = bx;
+//   bx > 64:       T = the largest divisor of bx in [8, 64], bulk tiles take
+//                  their updates bx/T steps at a time (rank bx, as in the reference);
+//   bx < 8:        T = the smallest multiple of bx in [8, 64] dividing n (the
+//                  8-wide DMMA atom: sub-atom panels are packed, as 3mm packs
+//                  sub-atom regions).
+// 0 when no such T exists (the graph schedule runs).
+int tile_for(int n, int bx) {
+  if (bx < 1 || n % bx) return 0;
+  if (bx >= kMinTile && bx <= kMaxTile) return bx;
+  if (bx > kMaxTile) {
+    for (int t = kMaxTile; t >= kMinTile; --t)
+      if (bx % t == 0) return t;
+    return 0;
+  }
+  for (int t = bx * ((kMinTile + bx - 1) / bx); t <= kMaxTile; t += bx)
+    if (n % t == 0) return t;
+  return 0;
+}
+
+// The reference's trailing row tile by (kernels.cpp:205-216) is the row
+// extent of the update / solve tasks, packed to at least
+// max(kMinRegion, kMinTaskElems / T) rows (one 16-row strip per warp, and
+// enough output elements per task for narrow tiles): a CTA owns adjacent
+// by-row regions, as the GEMM packs sub-atom knob regions.
+int region_rows(int by, int T) {
+  if (by < 1 || T < 1) return 0;
+  const char* v = std::getenv("TT_DAG_MINROWS");  // tuning aid: minimum task rows
+  const int mr = v && std::atoi(v) > 0 ? std::atoi(v) : kMinRegion;
+  const int lo = std::max(mr, (kMinTaskElems + T - 1) / T);
+  return by >= lo ? by : by * ((lo + by - 1) / by);
+}
+
 bool eligible(int n, int by, int bx) {
-  if (bx < kMinTile || bx > kMaxTile || n % bx || by < 1 || n % by) return false;
+  if (by < 1 || n % by || tile_for(n, bx) == 0) return false;
   return count_tasks(false, n, by, bx) <= kMaxTasks;
 }
 
@@ -1567,12 +1880,22 @@ GemmMerge gemm_merge() {
 // Chunk depth: steps per bulk GEMM task, K = d*T ~ 200 (TT_DAG_CHUNK=d
 // overrides; 1 = step-by-step updates), capped by the shared memory the q
 // stacked B tiles take.
-int chunk_depth(int bx) {
-  const int tp = (bx + 7) / 8 * 8;
-  const int cap = std::max(1, kBudget / (tp * std::max(bstride(tp, true), bstride(tp, false))));
+// TT_DAG_PIPE=0: GEMM tasks on the register path (A/B aid); default gemm_pipe.
+bool pipe_gemm() {
+  const char* v = std::getenv("TT_DAG_PIPE");  // read per workspace / launch (tests vary it)
+  return !(v && v[0] == '0');
+}
+
+int chunk_depth(int n, int bx) {
+  const int T = tile_for(n, bx);
+  if (T == 0) return 1;
+  const int tp = (T + 7) / 8 * 8;
+  // the q stacked B tiles share the CTA's shared memory with gemm_pipe's rings
+  const int room = kBudget - (pipe_gemm() ? ring_doubles(tp / 8) + 2 : 0);
+  const int cap = std::max(1, room / (tp * std::max(bstride(tp, true), bstride(tp, false))));
   const char* v = std::getenv("TT_DAG_CHUNK");  // read per workspace (tests vary it)
   const int forced = v ? std::atoi(v) : 0;
-  const int d = forced >= 1 ? forced : (200 + bx / 2) / bx;
+  const int d = forced >= 1 ? forced : bx > kMaxTile ? bx / T : (200 + T / 2) / T;
   return std::max(1, std::min({d, cap, 0xFFFF / 2}));
 }
 
@@ -1602,8 +1925,10 @@ int chunk_depth(int bx) {
 // single step) stage structure changes (dag_factor.cuh).
 // Returns urgent ++ bulk; *n_urgent = urgent count.
 std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
+  const int d = chunk_depth(n, bx);
+  bx = tile_for(n, bx);
+  by = region_rows(by, bx);
   const int T = bx, nt = n / bx;
-  const int d = chunk_depth(bx);
   const int band = urgent_band();
   const GemmMerge gm = gemm_merge();
   struct Keyed {
@@ -1722,12 +2047,16 @@ std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent) {
 cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   int nurg = 0;
   const std::vector<int4> tasks = build_tasks(chol, n, by, bx, &nurg);
-  const int nt = n / bx;
+  w->T = tile_for(n, bx);
+  const int nt = n / w->T;
   w->ntasks = static_cast<int>(tasks.size());
   w->nurgent = nurg;
-  w->chunk = chunk_depth(bx);
-  w->nsteps = n / bx;
-  w->cnt_bytes = (static_cast<size_t>(nt) * nt + 3) * sizeof(int);
+  w->chunk = chunk_depth(n, bx);
+  w->pipe = pipe_gemm() ? 1 : 0;
+  w->nsteps = nt;
+  // nt*nt tile counters, then: urgent next, abort flag, bulk next, and the
+  // watchdog record {recorded, cta, counter, need, seen} (kDiagInts)
+  w->cnt_bytes = (static_cast<size_t>(nt) * nt + 3 + kDiagInts) * sizeof(int);
   cudaError_t e = cudaMalloc(&w->tasks, tasks.size() * sizeof(int4));
   if (e != cudaSuccess) return e;
   e = cudaMemcpy(w->tasks, tasks.data(), tasks.size() * sizeof(int4), cudaMemcpyHostToDevice);
@@ -1756,6 +2085,19 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   return cudaSuccess;
 }
 
+std::string watchdog_info(const Workspace& w) {
+  if (!w.cnt) return {};
+  const int nt = w.nsteps;
+  int rec[kDiagInts] = {};
+  if (cudaMemcpy(rec, w.cnt + static_cast<size_t>(nt) * nt + 3, sizeof(rec),
+                 cudaMemcpyDeviceToHost) != cudaSuccess || rec[0] == 0)
+    return {};
+  char buf[160];
+  std::snprintf(buf, sizeof(buf), "cta %d waited on tile (%d, %d) for %d rows, saw %d", rec[1],
+                rec[2] / nt, rec[2] % nt, rec[3], rec[4]);
+  return buf;
+}
+
 void destroy(Workspace* w) {
   if (w->tasks) cudaFree(w->tasks);
   if (w->cnt) cudaFree(w->cnt);
@@ -1764,10 +2106,16 @@ void destroy(Workspace* w) {
   *w = Workspace{};
 }
 
-cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long ld, int bx,
-                    int* info, cudaStream_t s) {
-  const int nt = n / bx;
-  cudaError_t e = cudaMemsetAsync(w.cnt, 0, w.cnt_bytes, s);
+cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long ld, int* info,
+                    cudaStream_t s) {
+  const int bx = w.T, nt = n / bx;
+  static const bool nodeps = [] {
+    const char* v = std::getenv("TT_DAG_NODEPS");
+    return v && v[0] == '1';
+  }();
+  const size_t tiles = static_cast<size_t>(nt) * nt * sizeof(int);
+  cudaError_t e = cudaMemsetAsync(w.cnt, nodeps ? 0x3F : 0, tiles, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(w.cnt + static_cast<size_t>(nt) * nt, 0, w.cnt_bytes - tiles, s);
   if (e != cudaSuccess) return e;
   Params prm;
   prm.a = a;
@@ -1785,6 +2133,12 @@ cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long l
   prm.nurgent = w.nurgent;
   prm.nuw = w.nuw;
   prm.pf_mask = prefetch_mask();
+  prm.nodeps = nodeps ? 1 : 0;
+  prm.fence = [] {
+    const char* v = std::getenv("TT_DAG_FENCE");
+    return v && v[0] == '1' ? 1 : 0;
+  }();
+  prm.pipe = w.pipe;  // fixed at create(): the chunk depth's shared-memory budget depends on it
   prm.d = w.chunk;
   // measured default: Cholesky (whose bulk GEMMs feed the next step's strips
   // directly) gains 2% from publishing each strip at once, LU does not

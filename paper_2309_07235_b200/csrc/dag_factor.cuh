@@ -21,6 +21,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <string>
 #include <vector>
 
 namespace tt {
@@ -73,12 +74,17 @@ __host__ __device__ inline int stages_total(int m, int d, int o) {
 // the warp-register code of diag_factor.cuh, <= 64).
 constexpr int kMaxTile = 64;
 constexpr int kMinTile = 8;
+constexpr int kMinRegion = 128;      // rows per update / solve task, at least ...
+constexpr int kMinTaskElems = 5120;  // ... and output elements (rows x T)
 constexpr long long kMaxTasks = 8LL << 20;
 
 // Watchdog: a dependency wait longer than this aborts the schedule with
 // info = kTimeout (a scheduling bug must never hang the GPU).
 constexpr long long kWatchdogNs = 4000000000LL;
 constexpr int kTimeout = -2147483647 - 1;  // INT_MIN
+// Ints after the abort flag kept for the watchdog record (see watchdog_info).
+constexpr int kDiagInts = 5;
+
 
 // Opts every persistent-kernel variant into its shared memory on the
 // current device (called per context: the attribute is per device).
@@ -86,6 +92,10 @@ cudaError_t configure_device();
 
 // True when the persistent schedule covers (n, by, bx).
 bool eligible(int n, int by, int bx);
+// Tile T the schedule runs for panel width bx (0: none), and the row extent
+// of its update / solve tasks for row tile by (see dag_factor.cu).
+int tile_for(int n, int bx);
+int region_rows(int by, int T);
 
 // Host-built task list in dependency-respecting priority order
 // (int4 {kind | j << 2, k, r0, r1}).
@@ -95,18 +105,20 @@ bool eligible(int n, int by, int bx);
 std::vector<int4> build_tasks(bool chol, int n, int by, int bx, int* n_urgent);
 
 // Chunk depth d used for (n, by, bx) (TT_DAG_CHUNK overrides; 1 = step by step).
-int chunk_depth(int bx);
+int chunk_depth(int n, int bx);
 
 struct Workspace {
   int4* tasks = nullptr;   // device task list
   int ntasks = 0;
-  int nsteps = 0;          // n / bx: walker steps (trace rows after the tasks)
+  int T = 0;               // tile (tile_for(n, bx))
+  int nsteps = 0;          // n / T: walker steps (trace rows after the tasks)
   int nurgent = 0;         // urgent-queue tasks (the first nurgent of the list)
   int nuw = 0;             // CTAs serving the urgent queue
   int* cnt = nullptr;      // nt*nt tile counters + urgent counter, abort flag, bulk counter
   size_t cnt_bytes = 0;
   int grid = 0;
   int chunk = 1;           // chunk depth d
+  int pipe = 1;            // GEMM tasks through the shared-memory pipeline (TT_DAG_PIPE)
   unsigned long long* trace = nullptr;  // TT_DAG_TRACE=1: per-task timestamps
   double* solve = nullptr;              // per-step diagonal reciprocals written by DIAG
 };
@@ -115,9 +127,13 @@ struct Workspace {
 cudaError_t create(Workspace* w, bool chol, int n, int by, int bx);
 void destroy(Workspace* w);
 
+// After a kTimeout: "cta C waited on tile (i, j) for N rows, saw V" (synchronous
+// read of the workspace; empty when nothing was recorded).
+std::string watchdog_info(const Workspace& w);
+
 // Enqueues counter reset + the persistent kernel on `s` (graph-capturable).
-cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long ld, int bx,
-                    int* info, cudaStream_t s);
+cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long ld, int* info,
+                    cudaStream_t s);
 
 }  // namespace dag
 }  // namespace tt

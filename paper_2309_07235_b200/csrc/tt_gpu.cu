@@ -267,10 +267,8 @@ int get_graph(tt_ctx* ctx, const GraphKey& key, Enqueue&& enq, cudaGraphExec_t* 
 // graph (schedules.cu); otherwise the persistent tile-DAG kernel
 // (dag_factor.cu) runs whenever it covers (n, by, bx).
 bool use_dag_schedule(int n, int by, int bx) {
-  static const bool graph_only = [] {
-    const char* v = std::getenv("TT_FACTOR_SCHEDULE");
-    return v && std::strcmp(v, "graph") == 0;
-  }();
+  const char* v = std::getenv("TT_FACTOR_SCHEDULE");  // per call: tests switch it
+  const bool graph_only = v && std::strcmp(v, "graph") == 0;
   return !graph_only && tt::dag::eligible(n, by, bx);
 }
 
@@ -292,7 +290,7 @@ int factor_graph(tt_ctx* ctx, int kernel, double* a, int n, long long ld, int by
         if (dag) {
           ctx->dag_last = w;
           st->launches += 1;
-          return tt::dag::enqueue(*w, chol, a, n, ld, bx, ctx->info, ctx->stream);
+          return tt::dag::enqueue(*w, chol, a, n, ld, ctx->info, ctx->stream);
         }
         const tt::Streams ss{ctx->stream, ctx->stream2, ctx->fork, ctx->join};
         return !chol ? tt::enqueue_lu(ctx->tmaps, a, n, ld, by, bx, ctx->ws, ctx->info, ss, st)
@@ -380,8 +378,11 @@ int enqueue_run(tt_ctx* ctx, const int* cfg, cudaEvent_t ev_start, cudaEvent_t e
 
 int numeric_status(tt_ctx* ctx, int info, int* fail_index) {
   if (info == tt::kNoFailure) return TT_OK;
-  if (info == tt::dag::kTimeout)
-    return fail(ctx, TT_EDEVICE, "persistent schedule watchdog: dependency wait timed out");
+  if (info == tt::dag::kTimeout) {
+    const std::string why = ctx->dag_last ? tt::dag::watchdog_info(*ctx->dag_last) : std::string();
+    return fail(ctx, TT_EDEVICE, "persistent schedule watchdog: dependency wait timed out%s%s",
+                why.empty() ? "" : ": ", why.c_str());
+  }
   if (fail_index) *fail_index = info;
   if (ctx->kernel == TT_KERNEL_CHOLESKY)
     return fail(ctx, TT_ENUMERIC, "cholesky: non-positive diagonal at row %d", info);
@@ -1018,7 +1019,17 @@ int tt_dag_tasks(int kernel, int n, int by, int bx, int* out, int cap) {
 
 int tt_dag_chunk_depth(int n, int by, int bx) {
   if (!tt::dag::eligible(n, by, bx)) return -1;
-  return tt::dag::chunk_depth(bx);
+  return tt::dag::chunk_depth(n, bx);
+}
+
+int tt_dag_tile(int n, int by, int bx) {
+  if (!tt::dag::eligible(n, by, bx)) return -1;
+  return tt::dag::tile_for(n, bx);
+}
+
+int tt_dag_region_rows(int n, int by, int bx) {
+  if (!tt::dag::eligible(n, by, bx)) return -1;
+  return tt::dag::region_rows(by, tt::dag::tile_for(n, bx));
 }
 
 int tt_dag_urgent(int kernel, int n, int by, int bx) {

@@ -192,7 +192,8 @@ def test_task_order_and_coverage(kernel, n, by, bx):
     tasks = _lib.dag_tasks(kernel, n, by, bx)
     assert tasks is not None
     chol = kernel == "cholesky"
-    T, nt = bx, n // bx
+    T = _lib.dag_tile(n, by, bx)
+    nt = n // T
     d = _lib.dag_chunk_depth(n, by, bx)
     assert not np.any((tasks[:, 0] & 3) == DIAG)  # DIAG belongs to the walker
     cnt = np.zeros((nt, nt), dtype=np.int64)
@@ -310,7 +311,7 @@ def test_task_semantics_reproduce_reference(kernel, n, by, bx):
     chol = kernel == "cholesky"
     a0 = oracle.gen_spd(n, 5)
     nurg = _lib.load().tt_dag_urgent(_lib.KERNEL_IDS[kernel], n, by, bx)
-    out = run_tasks_numpy(a0, _lib.dag_tasks(kernel, n, by, bx), bx, chol, nurg,
+    out = run_tasks_numpy(a0, _lib.dag_tasks(kernel, n, by, bx), _lib.dag_tile(n, by, bx), chol, nurg,
                           _lib.dag_chunk_depth(n, by, bx))
     ref = a0.copy()
     if chol:
@@ -324,7 +325,30 @@ def test_task_semantics_reproduce_reference(kernel, n, by, bx):
         assert np.abs(out - ref).max() <= 1e-10 * np.abs(ref).max()
 
 
-def test_ineligible_configs_use_graph_schedule():
-    assert _lib.dag_tasks("lu", 2000, 400, 5) is None     # tile below the DMMA atom
-    assert _lib.dag_tasks("lu", 2000, 400, 80) is None    # tile above 64 (graph schedule)
-    assert _lib.dag_tasks("cholesky", 4000, 4000, 4000) is None
+def test_knob_mapping():
+    """bx -> tile T and chunk depth, by -> task rows (dag_factor.cu tile_for / region_rows)."""
+    assert _lib.dag_tile(2000, 400, 40) == 40                  # 8 <= bx <= 64: T = bx
+    assert _lib.dag_tile(2000, 400, 80) == 40                  # wider panels: divisor <= 64 ...
+    assert _lib.dag_chunk_depth(2000, 400, 80) == 2            # ... and rank-bx bulk updates
+    assert _lib.dag_tile(4000, 250, 250) == 50
+    assert 4 <= _lib.dag_chunk_depth(4000, 250, 250) <= 5   # bx/T = 5, capped by shared memory
+    assert _lib.dag_tile(4000, 4000, 4000) == 50
+    assert _lib.dag_tile(2000, 400, 5) == 10                   # sub-atom panels packed
+    assert _lib.dag_tile(4000, 250, 1) == 8
+    assert _lib.dag_region_rows(2000, 16, 40) == 128           # small row tiles packed
+    assert _lib.dag_region_rows(2000, 50, 40) == 150
+    assert _lib.dag_region_rows(2000, 400, 40) == 400
+    assert _lib.dag_region_rows(4000, 1, 8) == 640              # narrow tiles: >= 5120 elements
+    assert _lib.dag_tasks("cholesky", 4000, 1, 1) is not None
+    assert _lib.dag_tasks("lu", 67 * 3, 3, 67) is None         # prime panel > 64: graph schedule
+    assert _lib.dag_tile(67 * 3, 3, 67) is None
+
+
+@pytest.mark.parametrize("kernel,n,by,bx", [("lu", 160, 16, 80), ("cholesky", 160, 5, 160),
+                                            ("lu", 96, 96, 4), ("cholesky", 120, 10, 2),
+                                            ("lu", 200, 8, 100), ("cholesky", 100, 100, 1)])
+def test_mapped_knobs_order_and_semantics(kernel, n, by, bx):
+    """Knob settings outside 8..64 run the persistent schedule with the mapped tile."""
+    assert _lib.dag_tasks(kernel, n, by, bx) is not None
+    test_task_order_and_coverage(kernel, n, by, bx)
+    test_task_semantics_reproduce_reference(kernel, n, by, bx)

@@ -2,7 +2,8 @@
 urgent/bulk queues) against the oracle.
 
 Covers what the reference's kernel tests pin (kernels_test.cpp:159-316), on
-knob settings that run the persistent kernel (8 <= bx <= 64): parity over a
+every knob setting (all run the persistent kernel; panel widths outside 8..64
+through the mapped tile, dag_factor.cu tile_for): parity over a
 knob sweep, failure predicates at chosen columns (vanishing pivot, non-positive
 diagonal — NaN passes), bitwise determinism under the dynamic task schedule,
 the upper triangle of Cholesky never written, the walker-only (n = bx) and
@@ -14,7 +15,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_2309_07235_b200 import NumericalError, _lib, cholesky_factor_inplace, lu_factor_inplace
+from paper_2309_07235_b200 import NumericalError, _lib, cholesky_factor_inplace, cholesky_tiled, lu_factor_inplace
 
 pytestmark = pytest.mark.gpu
 
@@ -32,7 +33,7 @@ def rel(x, ref):
 
 
 N = 200
-BXS = [b for b in divisors(N) if 8 <= b <= 64]           # 8, 10, 20, 25, 40, 50
+BXS = divisors(N)  # every panel width runs the persistent kernel (mapped tile outside 8..64)
 BYS = [1, 5, 8, 25, 40, 100, 200]
 
 
@@ -147,17 +148,24 @@ def test_bitwise_determinism_dynamic_schedule(gpu_ctx):
         assert all(np.array_equal(outs[0], o) for o in outs[1:]), (by, bx)
 
 
-def test_graph_and_dag_schedules_agree(gpu_ctx):
-    """The same knob setting through both schedules (fresh processes pick
-    TT_FACTOR_SCHEDULE at load; here: a DAG-eligible setting vs a nearby
-    graph-only panel width, both against the oracle)."""
+@pytest.mark.parametrize("by,bx", [(40, 40), (40, 100), (8, 200), (50, 4)])
+def test_graph_and_dag_schedules_agree(gpu_ctx, monkeypatch, by, bx):
+    """The same knob setting through both schedules (TT_FACTOR_SCHEDULE=graph
+    forces the launch-per-kernel graph), both against the oracle; panel widths
+    outside 8..64 run the persistent schedule with the mapped tile."""
     a = oracle.gen_spd(N, 5)
     ref = a.copy()
     oracle.lu_factor_inplace(ref, N, N)
+    assert on_dag("lu", N, by, bx)
     w_dag = a.copy()
-    lu_factor_inplace(w_dag, 40, 40, ctx=gpu_ctx)
-    assert not on_dag("lu", N, 40, 100)
+    lu_factor_inplace(w_dag, by, bx, ctx=gpu_ctx)
+    monkeypatch.setenv("TT_FACTOR_SCHEDULE", "graph")
     w_graph = a.copy()
-    lu_factor_inplace(w_graph, 40, 100, ctx=gpu_ctx)
+    lu_factor_inplace(w_graph, by, bx, ctx=gpu_ctx)
+    l_graph = cholesky_tiled(a, by, bx, ctx=gpu_ctx)
+    monkeypatch.delenv("TT_FACTOR_SCHEDULE")
+    l_dag = cholesky_tiled(a, by, bx, ctx=gpu_ctx)
     assert rel(w_dag, ref) <= 1e-10 and rel(w_graph, ref) <= 1e-10
     assert rel(w_dag, w_graph) <= 1e-10
+    assert oracle.cholesky_residual(a, l_dag) <= 1e-12
+    assert oracle.cholesky_residual(a, l_graph) <= 1e-12

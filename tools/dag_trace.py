@@ -21,7 +21,7 @@ for _ in range(3):
     r.run((by, bx), want_output=False)
 tasks = _lib.dag_tasks(kern, n, by, bx)
 nt = len(tasks)
-nsteps = n // bx
+nsteps = n // _lib.dag_tile(n, by, bx)
 trall = np.zeros((nt + nsteps, 8), dtype=np.uint64)
 got = ctx.lib.tt_dag_trace(ctx.handle, trall.ctypes.data_as(ctypes.c_void_p), nt + nsteps)
 tr = trall[:nt]
