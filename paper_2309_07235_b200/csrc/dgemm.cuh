@@ -55,20 +55,30 @@ struct GemmArgs {
 
 template <int BM, int BN, bool BT>
 struct GemmShape {
-  // Warp tiles up to 32 x 64 (64 fp64 accumulators per lane) and at most 4
-  // consumer warps + 1 producer: the register file is split across the 4
-  // SM sub-partitions (16K regs each), so >4 warps of ~200 registers do not
-  // fit one CTA.  128 x 128 regions are therefore swept as 128 x 64 tiles.
+  // Warp tiles up to 32 x 64 (64 fp64 accumulators per lane).  A DMMA warp
+  // carries a fixed issue stall after every DMMA, so one consumer warp per SM
+  // sub-partition cannot keep the fp64 tensor pipe busy next to its fragment
+  // loads (72% pipe-active with 4 warps of 32 x 64, profiles/ncu_r02_3mm_xl.txt):
+  // tiles of >= 128 x 64 run 8 consumer warps (two per sub-partition) —
+  // 4 x 2 warps of 32 x 64 (128 x 128), 4 x 2 of 32 x 32 (128 x 64),
+  // 2 x 4 of 32 x 32 (64 x 128) — and 64 x 64 runs 2 x 2 of 32 x 32.
   static constexpr int WTM = BM < 32 ? BM : 32;
-  static constexpr int WTN = BN < 64 ? BN : 64;
   static constexpr int WGM = BM / WTM;
-  static constexpr int WGN = BN / WTN;
+  static constexpr int WGN = (BM * BN >= 128 * 64) ? 8 / WGM
+                             : (BM == 64 && BN == 64) ? 2
+                             : (BN < 64 ? 1 : BN / 64);
+  static constexpr int WTN = BN / WGN;
   static constexpr int MF = WTM / 8;
   static constexpr int NF = WTN / 8;
   static constexpr int NCW = WGM * WGN;
-  static constexpr int THREADS = (NCW + 1) * 32;
-  static_assert(NCW <= 4, "at most 4 consumer warps");
-  static constexpr int STAGES = (BM + BN) >= 192 ? 4 : 6;
+  // 8 consumer warps: no separate producer warp (ptxas budgets registers
+  // per 4-warp group: a 9th warp would cap every thread at 168 registers);
+  // consumer warp 0's lane 0 issues the TMA loads in line, STAGES-1 ahead.
+  // These variants have no C prefetch (beta = 1 loads C directly).
+  static constexpr bool INLINE_TMA = NCW == 8;
+  static constexpr int THREADS = (NCW + (INLINE_TMA ? 0 : 1)) * 32;
+  static_assert(NCW <= 8, "at most 8 consumer warps");
+  static constexpr int STAGES = (BM + BN) >= 256 ? 5 : (BM + BN) >= 192 ? 4 : 6;
   static constexpr int A_BYTES = BM * kBK * 8;
   static constexpr int B_COLS = BT ? BN : (BN < 16 ? 16 : BN);  // NN boxes are 16 wide
   static constexpr int B_BYTES = B_COLS * kBK * 8;
@@ -80,6 +90,10 @@ struct GemmShape {
   static constexpr int C_LD = BN + 2;  // doubles per row of the C prefetch box
   static constexpr int C_BYTES = BM * C_LD * 8;
   static constexpr int SMEM = STAGES * STAGE_BYTES + C_BYTES + 2 * STAGES * 8 + 16 + 1024;
+  // without the C prefetch buffer (beta = 0, or c_tma off): the barriers
+  // move to its place, the kernel never touches sC
+  static constexpr int SMEM_NOC = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 16 + 1024;
+  static constexpr int SMEM_OPT = SMEM <= 227 * 1024 ? SMEM : SMEM_NOC;
 };
 
 // Byte offset of (row, 16B-chunk) in a tile of 128-byte rows written by TMA
@@ -97,12 +111,13 @@ __global__ void __launch_bounds__(GemmShape<BM, BN, BT>::THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const bool c_tma = !S::INLINE_TMA && p.beta && p.c_tma;
   double* sC = reinterpret_cast<double*>(smem + S::STAGES * S::STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES + S::C_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES +
+                                               (c_tma ? S::C_BYTES : 0));
   uint64_t* empty = full + S::STAGES;
   uint64_t* cfull = empty + S::STAGES;
   uint64_t* cempty = cfull + 1;
-  const bool c_tma = p.beta && p.c_tma;
 
   const int rid = blockIdx.x;
   const int ry = rid / p.nreg_x;
@@ -128,7 +143,7 @@ __global__ void __launch_bounds__(GemmShape<BM, BN, BT>::THREADS, 1)
   }
   __syncthreads();
 
-  if (warp == S::NCW) {  // ---------------- TMA producer ----------------
+  if (!S::INLINE_TMA && warp == S::NCW) {  // ---------------- TMA producer ----------------
     if (lane == 0) {
       prefetch_tmap(&tmA);
       prefetch_tmap(&tmB);
@@ -186,6 +201,49 @@ __global__ void __launch_bounds__(GemmShape<BM, BN, BT>::THREADS, 1)
   uint32_t phase = 0;
   uint32_t cphase = 0;
 
+  // in-line producer (INLINE_TMA; never with the C prefetch): the chunk
+  // stream of the tile loop below, issued STAGES-1 chunks ahead; issuing
+  // chunk g+STAGES-1 reuses chunk g-1's slot (every warp released it)
+  int q_t = 0, q_kc = 0, q_stage = 0;
+  uint32_t q_phase = 0;
+  auto issue_next = [&]() {
+    for (; q_t < nty * ntx; ++q_t, q_kc = 0) {
+      const int ty = q_t / ntx, tx = q_t - (q_t / ntx) * ntx;
+      const int ty0 = y0 + ty * BM, tx0 = x0 + tx * BN;
+      if (p.lower && (min(ty0 + BM, y1) - 1 + p.diag_off < tx0)) continue;
+      const int bs = BT ? 0 : ((p.b_c0 + tx0) & 1);
+      const int nbox = S::NBOX_B + ((bs && BN >= 16) ? 1 : 0);
+      const uint32_t tx_bytes = S::A_BYTES + (BT ? S::B_BYTES : nbox * (kBK * 128));
+      mbar_wait(&empty[q_stage], q_phase ^ 1);
+      uint8_t* sa = smem + q_stage * S::STAGE_BYTES;
+      uint8_t* sb = sa + S::A_BYTES;
+      mbar_arrive_expect_tx(&full[q_stage], tx_bytes);
+      tma_load_2d(sa, &tmA, &full[q_stage], p.a_c0 + q_kc * kBK, p.a_r0 + ty0);
+      if (BT) {
+        tma_load_2d(sb, &tmB, &full[q_stage], p.b_c0 + q_kc * kBK, p.b_r0 + tx0);
+      } else {
+        for (int j = 0; j < nbox; ++j)
+          tma_load_2d(sb + j * (kBK * 128), &tmB, &full[q_stage], p.b_c0 + tx0 - bs + 16 * j,
+                      p.b_r0 + q_kc * kBK);
+      }
+      if (++q_stage == S::STAGES) {
+        q_stage = 0;
+        q_phase ^= 1;
+      }
+      if (++q_kc == nk) {
+        q_kc = 0;
+        ++q_t;
+      }
+      return;
+    }
+  };
+  const bool producer_lane = S::INLINE_TMA && warp == 0 && lane == 0;
+  if (producer_lane) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int i = 0; i + 1 < S::STAGES; ++i) issue_next();
+  }
+
   for (int ty = 0; ty < nty; ++ty) {
     const int ty0 = y0 + ty * BM;
     const int ty1 = min(ty0 + BM, y1);
@@ -238,6 +296,7 @@ __global__ void __launch_bounds__(GemmShape<BM, BN, BT>::THREADS, 1)
 
       for (int kc = 0; kc < nk; ++kc) {
         mbar_wait(&full[stage], phase);
+        if (producer_lane) issue_next();
         const uint8_t* sa = smem + stage * S::STAGE_BYTES;
         const uint8_t* sb = sa + S::A_BYTES;
         // chunk-local valid k' window [klo_c, kvalid): masks the aligned-origin

@@ -32,10 +32,26 @@ int tile_edge(int reg) {
   return 128;
 }
 
-// Sub-atom knob regions (< 8) are packed: a CTA owns ceil(8/f) adjacent knob
-// regions so that it fills one 8-wide DMMA atom.
+// Knob region -> CTA region (one CTA per region, every output element one
+// full-K reduction by one CTA: the arithmetic per element is the same for
+// every mapping).  The knob's region edge f (the reference's outer tile,
+// kernels.cpp:91-111) is kept as the CTA edge inside [32, 128]; outside it:
+//   f < 32:  floor(64 / f) adjacent knob regions are packed into one CTA
+//            region (as the DMMA atom packs sub-8 regions), so a CTA never
+//            runs a warp tile narrower than 32;
+//   f > 128: the region is split into its s equal parts for the smallest
+//            divisor s of f with f / s <= 128 (so part edges stay on region
+//            edges), else into ceil(f / 128) near-equal parts — one CTA per
+//            part instead of one CTA sweeping a long region alone.
 int pack_region(int f, int extent) {
-  int r = f < 8 ? f * ((8 + f - 1) / f) : f;
+  int r = f;
+  if (f < 32) {
+    r = f * std::max(1, 64 / f);
+  } else if (f > 128) {
+    int s = (f + 127) / 128;
+    while (f % s && f / s >= 32) ++s;
+    r = f % s ? (f + (f + 127) / 128 - 1) / ((f + 127) / 128) : f / s;
+  }
   return std::max(1, std::min(r, extent));
 }
 
@@ -98,7 +114,6 @@ GemmPlan plan_gemm(int M, int N, int fy, int fx) {
   p.reg_x = pack_region(fx, N);
   p.bm = tile_edge(p.reg_y);
   p.bn = tile_edge(p.reg_x);
-  if (p.bm == 128 && p.bn == 128) p.bn = 64;  // largest variant is 128 x 64 (4 warps of 32 x 64)
   p.nreg_y = (M + p.reg_y - 1) / p.reg_y;
   p.nreg_x = (N + p.reg_x - 1) / p.reg_x;
   return p;
@@ -154,10 +169,10 @@ cudaError_t gemm(TmapCache& tc, const Operand& A, const Operand& B, bool b_trans
   args.c_sh = 0;
   const CUtensorMap* tcm = ta;
   const uintptr_t caddr = reinterpret_cast<uintptr_t>(c);
-  if (beta && (ldc % 2) == 0 && (caddr % 8) == 0) {
+  // (the 8-consumer-warp tiles, >= 128 x 64, issue TMA in line: no C prefetch)
+  if (beta && plan.bm * plan.bn < 128 * 64 && (ldc % 2) == 0 && (caddr % 8) == 0) {
     const int sh = (caddr % 16) ? 1 : 0;
-    const int bn_eff = plan.bm == 128 && plan.bn == 128 ? 64 : plan.bn;
-    const CUtensorMap* m = tc.get_plain(c - sh, M, N + sh, ldc, plan.bm, bn_eff + 2);
+    const CUtensorMap* m = tc.get_plain(c - sh, M, N + sh, ldc, plan.bm, plan.bn + 2);
     if (m) {
       tcm = m;
       args.c_tma = 1;

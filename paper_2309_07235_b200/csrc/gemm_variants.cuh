@@ -10,11 +10,13 @@ cudaError_t launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const C
                            const GemmArgs& args, long long grid, cudaStream_t stream) {
   using S = GemmShape<BM, BN, BT>;
   static std::atomic<unsigned long long> configured{0};  // per variant, one bit per device
-  const cudaError_t e = smem_optin(dgemm_kernel<BM, BN, BT>, S::SMEM, configured);
+  const cudaError_t e = smem_optin(dgemm_kernel<BM, BN, BT>, S::SMEM_OPT, configured);
   if (e != cudaSuccess) return e;
   if (grid <= 0) return cudaSuccess;
-  dgemm_kernel<BM, BN, BT><<<static_cast<unsigned>(grid), S::THREADS, S::SMEM, stream>>>(ta, tb, tc,
-                                                                                         args);
+  const bool c_tma = args.beta && args.c_tma;
+  if (c_tma && S::SMEM_OPT < S::SMEM) return cudaErrorInvalidValue;  // plan_gemm never asks
+  dgemm_kernel<BM, BN, BT><<<static_cast<unsigned>(grid), S::THREADS, c_tma ? S::SMEM : S::SMEM_NOC,
+                             stream>>>(ta, tb, tc, args);
   return cudaGetLastError();
 }
 
@@ -24,7 +26,7 @@ cudaError_t launch_variant(const CUtensorMap& ta, const CUtensorMap& tb, const C
     case 16: return launch_variant<BM, 16, BT>(ta, tb, tc, args, grid, stream);     \
     case 32: return launch_variant<BM, 32, BT>(ta, tb, tc, args, grid, stream);     \
     case 64: return launch_variant<BM, 64, BT>(ta, tb, tc, args, grid, stream);     \
-    case 128: return launch_variant<BM, (BM == 128 ? 64 : 128), BT>(ta, tb, tc, args, grid, stream); \
+    case 128: return launch_variant<BM, 128, BT>(ta, tb, tc, args, grid, stream); \
   }                                                                             \
   return cudaErrorInvalidValue;
 

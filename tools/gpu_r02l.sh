@@ -1,0 +1,8 @@
+#!/bin/bash
+# 3mm: 8-consumer-warp 128x128 tile: parity, random sweeps (LARGE, XL), BO best-found over seeds.
+cd "${GRAFT_REPO_ROOT:-.}"
+mkdir -p gpurun_out
+timeout -s KILL 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_xl.py tests/test_gpu_dropin.py -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
+timeout -s KILL 300 python tools/sweep3mm.py --size extralarge --samples 300 --max-seconds 100 2>&1 | tail -8
+timeout -s KILL 300 python tools/sweep3mm.py --size large --samples 300 --max-seconds 60 2>&1 | tail -8
+timeout -s KILL 1200 python tools/t1t8.py --kernel 3mm --size extralarge --evals 200 --workers 8 --seeds 1,2,3 --out gpurun_out/t1t8_3mm_xl_c.jsonl 2>&1 | tail -4
