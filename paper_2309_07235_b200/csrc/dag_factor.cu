@@ -734,6 +734,23 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
   const int total = ns * per;
   int issued = 0;
 
+  // Per-lane copy pattern of one item (16 rows x T columns in 16-byte
+  // vectors), the same for every item: vector v = lane + 32 u is row r_u,
+  // column pair c_u; offsets precomputed once per task (the integer work of
+  // the copy loop was 2-3 IMAD per DMMA).
+  constexpr int NVEC = (kStrip * HP + 31) / 32;
+  int goff[NVEC], soff[NVEC];
+  unsigned rowmask = 0;  // bit u: vector u in a valid column; row checked per strip
+  int vrow[NVEC];
+#pragma unroll
+  for (int u = 0; u < NVEC; ++u) {
+    const int e = lane + 32 * u, r = e / HP, c = 2 * (e - r * HP);
+    vrow[u] = e < kStrip * HP ? r : kStrip;
+    goff[u] = r * static_cast<int>(ld) + c;
+    soff[u] = r * SA + c;
+    if (e < kStrip * HP && c < T) rowmask |= 1u << u;
+  }
+
   int is_i = 0, is_kk = 0;  // strip / item of the next item to issue
   auto issue = [&](int y) {
     const int i = is_i, kk = is_kk;
@@ -742,11 +759,12 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
                         (kk < q ? static_cast<long long>(k0 + kk) * T : static_cast<long long>(jT));
     double* dst = ring + (y % R) * kSlot;
     if (vec) {
-#pragma unroll 4
-      for (int e = lane; e < kStrip * HP; e += 32) {
-        const int r = e / HP, c = 2 * (e - r * HP);
-        const bool valid = r < nr && c < T;
-        cp_async16_zfill(dst + r * SA + c, valid ? src + static_cast<long long>(r) * ld + c : p.a, valid);
+#pragma unroll
+      for (int u = 0; u < NVEC; ++u) {
+        if (vrow[u] < kStrip) {
+          const bool valid = ((rowmask >> u) & 1) && vrow[u] < nr;
+          cp_async16_zfill(dst + soff[u], valid ? src + goff[u] : p.a, valid);
+        }
       }
     } else {  // odd T: synchronous copies (visible after the consumer's __syncwarp)
       for (int e = lane; e < kStrip * Tp; e += 32) {
@@ -756,12 +774,41 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
     }
     cp_async_commit();
   };
+  // Task-start poll: one round trip checks the A and C dependencies of all
+  // of this warp's strips (lane = one counter); strips found satisfied skip
+  // their per-strip polls (in the bulk of the schedule the inputs of a task
+  // are final by the time it starts).  Bit i of a_ok / c_ok: strip i ready.
+  unsigned a_ok = 0, c_ok = 0;
+  {
+    const int ti_lo = first / T;
+    const int ti_hi = ns > 0 ? (min(r1, first + (ns - 1) * stride + kStrip) - 1) / T : ti_lo - 1;
+    const int ntile = ti_hi - ti_lo + 1;
+    bool tile_ok = false;  // lane d < ntile: tile row ti_lo + d, A dep; ntile <= d < 2 ntile: C dep
+    if (ntile > 0 && 2 * ntile <= 32 && ns <= 32) {
+      if (lane < 2 * ntile) {
+        const int i = ti_lo + (lane < ntile ? lane : lane - ntile);
+        const int* c = lane < ntile ? &p.cnt[i * p.nt + kl] : &p.cnt[i * p.nt + j];
+        const int need = lane < ntile ? need_final(p, kl, kl)
+                                      : need_before(p, min(i, j), j, k0);
+        tile_ok = ld_acquire(c) >= need;
+      }
+      const unsigned okm = __ballot_sync(0xffffffffu, tile_ok);
+      const unsigned am = okm & ((1u << ntile) - 1), cm = (okm >> ntile) & ((1u << ntile) - 1);
+      for (int i = 0; i < ns; ++i) {
+        const int rs = first + i * stride, re = min(r1, rs + kStrip);
+        const int t0 = rs / T - ti_lo, t1 = (re - 1) / T - ti_lo;
+        const unsigned need = ((2u << t1) - 1) & ~((1u << t0) - 1);
+        if ((am & need) == need) a_ok |= 1u << i;
+        if ((cm & need) == need) c_ok |= 1u << i;
+      }
+    }
+  }
   // issue items up to x + R - 1 in order; item x itself waits for its inputs
   // when `block_x` (false: only on abort)
   auto pump = [&](int x, bool block_x) -> bool {
     while (issued < total && issued < x + R) {
       const int y = issued, i = is_i, kk = is_kk;
-      if (kk == 0 || kk == q) {
+      if ((kk == 0 && !((a_ok >> i) & 1)) || (kk == q && !((c_ok >> i) & 1))) {
         const int rs = first + i * stride, re = min(r1, rs + kStrip);
         const bool blk = block_x && y == x;
         const bool ok = kk == 0 ? a_deps(p, rs, re, kl, blk) : strip_deps(p, rs, re, j, k0, -1, blk);
