@@ -3,9 +3,9 @@
 time-to-best (BASELINE.json metric).
 
 Headline workload (configs[2]): Cholesky, PolyBench EXTRALARGE N=4000, at the
-BO-tuned knob setting BENCH_CHOL_BLOCK = (by, bx) — the best configuration of the
-committed 1-GPU BayesOpt run (seed TUNE_SEED, TUNE_EVALS evaluations,
-profiles/tune_chol_xl_r02.json) — inputs gen_spd(4000, seed=1).  A step is one
+BO-tuned knob setting BENCH_CHOL_BLOCK = (by, bx) — the best configuration found by
+the committed 1-GPU BayesOpt runs (seeds TUNE_SEEDS, TUNE_EVALS evaluations each,
+profiles/t1t8_chol_xl_r02b.jsonl) — inputs gen_spd(4000, seed=1).  A step is one
 in-place factorisation of one resident input: ONE launch of the persistent
 tile-DAG kernel (paper_2309_07235_b200/csrc/dag_factor.cu).  Inputs cycle through
 a ring of W+K distinct device copies (128 MB each: larger than the 126 MB L2, so
@@ -13,9 +13,10 @@ every step starts L2-cold), no restore copy inside the timed region.
 
 value    = (1/3) n^3 flop per step x steps x ranks / max-over-ranks device time
            (CUDA events on the launching stream)
-tuning   = a LIVE 1-GPU BayesOpt run in this process (same seed / budget as the
-           committed one): time_to_best_s = elapsed_s of its first record reaching
-           its final best, plus the config it found (SURVEY 8e definition)
+tuning   = LIVE 1-GPU BayesOpt runs in this process (same seeds / budget as the
+           committed ones): per run time_to_best_s = elapsed_s of its first record
+           reaching its final best, plus the config it found (SURVEY 8e definition);
+           tuning_scale = the committed T1/T8 virtual-clock results (tools/t1t8.py)
 e2e      = the same metric through the C ABI with pinned host buffers (H2D +
            factor + D2H every step): tt_cholesky_factor_batch, the pipelined batch
            drop-in; the one-call-per-matrix tt_cholesky_factor_inplace beside it
@@ -56,8 +57,8 @@ FP64_PEAK_TFLOPS = 37.05  # measured DMMA m8n8k4 issue rate (profiles/fp64_peak_
 FP64_PEAK_SOURCE = "measured: DMMA issue-rate microbenchmark, 148 SMs @1965 MHz (profiles/fp64_peak_r01.jsonl); cuBLAS DGEMM 8192^3 = 35.45"
 METRIC = "fp64 GFLOP/s of best-tuned config (% of B200 fp64 peak); tuning time-to-best"
 BENCH_N = 4000
-BENCH_CHOL_BLOCK = (250, 40)  # (by, bx): best of the committed BO run (profiles/tune_chol_xl_r02.json)
-TUNE_SEED = 1
+BENCH_CHOL_BLOCK = (1000, 40)  # (by, bx): best of the committed 3-seed BO runs (profiles/t1t8_chol_xl_r02b.jsonl)
+TUNE_SEEDS = (1, 2, 3)
 TUNE_EVALS = 60
 WORKLOAD = "cholesky_extralarge_bo_tuned"
 
@@ -66,7 +67,7 @@ def bench_config():
     """The config dict both arms print (identical keys and values)."""
     by, bx = BENCH_CHOL_BLOCK
     return {"workload": WORKLOAD, "kernel": "cholesky", "n": BENCH_N, "by": by, "bx": bx,
-            "tuner": "bayesopt", "tuning_seed": TUNE_SEED, "tuning_evals": TUNE_EVALS}
+            "tuner": "bayesopt", "tuning_seeds": list(TUNE_SEEDS), "tuning_evals": TUNE_EVALS}
 
 
 def lu_flops(n: int) -> float:
@@ -257,21 +258,32 @@ def cpu_baseline_single(a, by, bx):
 # ------------------------------------------------------------------ GPU arm
 
 def live_tuning(local):
-    """1-GPU BayesOpt on the headline case: time-to-best and the config found."""
+    """1-GPU BayesOpt on the headline case, one run per seed (same budget):
+    time-to-best (elapsed_s of the first record reaching the run's
+    final best) and the config each run found."""
     from paper_2309_07235_b200 import tuning
-    t0 = time.perf_counter()
-    recs, total = tuning.run_tuning_measured("bayesopt", "cholesky", "extralarge", TUNE_SEED,
-                                             TUNE_EVALS, devices=(local,))
-    wall = time.perf_counter() - t0
-    best = tuning.best_record(recs)
-    return {"tuner": "bayesopt", "seed": TUNE_SEED, "evals": len(recs), "devices": 1,
+    runs = []
+    for seed in TUNE_SEEDS:
+        t0 = time.perf_counter()
+        recs, total = tuning.run_tuning_measured("bayesopt", "cholesky", "extralarge", seed,
+                                                 TUNE_EVALS, devices=(local,))
+        wall = time.perf_counter() - t0
+        best = tuning.best_record(recs)
+        runs.append({"seed": seed, "evals": len(recs), "time_to_best_s": best.elapsed_s,
+                     "tuning_s": total, "wall_s_incl_setup": wall,
+                     "best_config": list(best.config), "best_ms": best.runtime_s * 1e3,
+                     "best_pct_of_fp64_peak": 100 * chol_flops(BENCH_N) / best.runtime_s / 1e12
+                     / FP64_PEAK_TFLOPS,
+                     "host_ask_s_total": sum(r.ask_s for r in recs)})
+    top = min(runs, key=lambda r: r["best_ms"])
+    return {"tuner": "bayesopt", "devices": 1, "evals_per_run": TUNE_EVALS,
             "protocol": "reference measure(): 1 warm-up + median of 3, CUDA events",
-            "time_to_best_s": best.elapsed_s, "tuning_s": total, "wall_s_incl_setup": wall,
-            "best_config": list(best.config), "best_ms": best.runtime_s * 1e3,
-            "best_pct_of_fp64_peak": 100 * chol_flops(BENCH_N) / best.runtime_s / 1e12 / FP64_PEAK_TFLOPS,
-            "host_ask_s_total": sum(r.ask_s for r in recs),
+            "runs": runs, "best_config": top["best_config"], "best_ms": top["best_ms"],
+            "best_pct_of_fp64_peak": top["best_pct_of_fp64_peak"],
+            "time_to_best_s_median": float(np.median([r["time_to_best_s"] for r in runs])),
             "committed_config": list(BENCH_CHOL_BLOCK),
-            "found_committed_config": list(best.config) == list(BENCH_CHOL_BLOCK)}
+            "runs_finding_committed_config": sum(r["best_config"] == list(BENCH_CHOL_BLOCK)
+                                                 for r in runs)}
 
 
 def run_gpu_arm(args, rank, world, local):
@@ -398,7 +410,8 @@ def run_gpu_arm(args, rank, world, local):
                          "peak_source": FP64_PEAK_SOURCE},
             "schedule": sched,
             "tuning": tuning,
-            "time_to_best_s": tuning["time_to_best_s"] if tuning else None,
+            "time_to_best_s": tuning["time_to_best_s_median"] if tuning else None,
+            "tuning_scale": committed_tuning_scale(),
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": n * n * 8,
                     "d2h_bytes_per_step": n * n * 8, "steps": e2e_steps,
                     "api": "tt_cholesky_factor_batch (C ABI, pipelined batch of cholesky_factor_inplace)",
@@ -414,6 +427,36 @@ def run_gpu_arm(args, rank, world, local):
         if cpu is not None:
             line["cpu_baseline"] = cpu
     return line, ctx
+
+
+def committed_tuning_scale():
+    """T1/T8 time-to-best from the committed virtual-clock runs
+    (tools/t1t8.py: 1 and 8 evaluators emulated on ONE B200, every evaluation
+    measured for real, the host's ask time charged serially; no 8-GPU node was
+    available).  Reported as committed evidence, not re-measured by this run."""
+    out = {}
+    for key, pat in (("mm3_extralarge_bo200", "t1t8_3mm_xl_r02*.jsonl"),
+                     ("cholesky_extralarge_bo60", "t1t8_chol_xl_r02*.jsonl")):
+        files = sorted((ROOT / "profiles").glob(pat))
+        if not files:
+            continue
+        rows = [json.loads(x) for x in files[-1].read_text().splitlines() if x.strip()]
+        runs = [r for r in rows if not r.get("summary")]
+        summ = next((r for r in rows if r.get("summary")), {})
+        out[key] = {
+            "file": f"profiles/{files[-1].name}",
+            "method": "virtual clock: W evaluators emulated on one B200 (tt_tune_virtual), real "
+                      "per-eval GPU times, serial host ask time",
+            "seeds": [r["seed"] for r in runs],
+            "T1_s": [r["T1_s"] for r in runs],
+            "T8_s": [r["TW_s"] if r["TW_s"] != float("inf") else None for r in runs],
+            "T8_within1pct_s": [r.get("TW_within1pct_s") for r in runs],
+            "median_T1_over_T8": summ.get("median_ratio"),
+            "median_T1_over_T8_within1pct": summ.get("median_ratio_within1pct"),
+            "best1_pct_of_fp64_peak": [r.get("best1_pct_of_fp64_peak") for r in runs],
+            "best8_pct_of_fp64_peak": [r.get("bestW_pct_of_fp64_peak") for r in runs],
+        }
+    return out or None
 
 
 def ncu_traffic(workload: str):
@@ -440,13 +483,16 @@ def schedule_info(lib, kid, n, by, bx):
 
 EXTRA_CASES = [
     # (name, kernel case args, config, flops, how the config was chosen)
-    ("lu_large_fixed_block", ("lu", 2000), (200, 40), lu_flops(2000),
-     "configs[1]: fixed block, the fastest of the N=2000 knob sweep"),
-    ("lu_extralarge", ("lu", 4000), (250, 40), lu_flops(4000), "best of the N=4000 sweep"),
-    ("mm3_large_fixed_tile", ("3mm", 800, 900, 1000, 1100, 1200), (100, 125, 125, 120, 32, 60),
-     mm3_flops(800, 900, 1000, 1100, 1200), "configs[0]: fixed tile config (grid search)"),
-    ("mm3_extralarge", ("3mm", 1600, 1800, 2000, 2200, 2400), (64, 125, 125, 300, 64, 240),
-     mm3_flops(1600, 1800, 2000, 2200, 2400), "grid-searched config"),
+    ("lu_large_fixed_block", ("lu", 2000), (400, 40), lu_flops(2000),
+     "configs[1]: fixed block, the fastest of the N=2000 knob sweep (profiles/sweep_lu2000_r02.jsonl)"),
+    ("lu_extralarge", ("lu", 4000), (1000, 40), lu_flops(4000),
+     "best of the N=4000 knob sweep (profiles/sweep_lu4000_r02.jsonl)"),
+    ("mm3_large_fixed_tile", ("3mm", 800, 900, 1000, 1100, 1200), (100, 40, 1000, 300, 16, 120),
+     mm3_flops(800, 900, 1000, 1100, 1200),
+     "configs[0]: one fixed tile config, the best of a 300-sample random sweep"),
+    ("mm3_extralarge", ("3mm", 1600, 1800, 2000, 2200, 2400), (2, 1000, 1000, 4, 1, 2),
+     mm3_flops(1600, 1800, 2000, 2200, 2400),
+     "configs[3]: best config found by the committed 200-eval BayesOpt runs (profiles/t1t8_3mm_xl_r02a.jsonl, seed 2)"),
 ]
 
 

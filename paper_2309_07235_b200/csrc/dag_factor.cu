@@ -148,6 +148,8 @@ __device__ bool wait_ge(const Params& p, const int* addr, int need) {
             p.abort[4] = static_cast<int>(addr - p.cnt);
             p.abort[5] = need;
             p.abort[6] = ld_relaxed(addr);
+            p.abort[7] = ld_relaxed(p.next);      // urgent queue position
+            p.abort[8] = ld_relaxed(p.next + 2);  // bulk queue position
           }
           atomicExch(p.abort, 2);
           atomicMin(p.info, kTimeout);
@@ -2102,13 +2104,15 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   w->pipe = pipe_gemm() ? 1 : 0;
   w->nsteps = nt;
   // nt*nt tile counters, then: urgent next, abort flag, bulk next, and the
-  // watchdog record {recorded, cta, counter, need, seen} (kDiagInts)
+  // watchdog record {recorded, cta, counter, need, seen, urgent pos, bulk pos} (kDiagInts)
   w->cnt_bytes = (static_cast<size_t>(nt) * nt + 3 + kDiagInts) * sizeof(int);
   cudaError_t e = cudaMalloc(&w->tasks, tasks.size() * sizeof(int4));
   if (e != cudaSuccess) return e;
   e = cudaMemcpy(w->tasks, tasks.data(), tasks.size() * sizeof(int4), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return e;
   e = cudaMalloc(&w->cnt, w->cnt_bytes);
+  if (e != cudaSuccess) return e;
+  e = cudaMemset(w->cnt, 0, w->cnt_bytes);
   if (e != cudaSuccess) return e;
   e = cudaMalloc(&w->solve, static_cast<size_t>(nt) * kSolveSlot * sizeof(double));
   if (e != cudaSuccess) return e;
@@ -2139,9 +2143,12 @@ std::string watchdog_info(const Workspace& w) {
   if (cudaMemcpy(rec, w.cnt + static_cast<size_t>(nt) * nt + 3, sizeof(rec),
                  cudaMemcpyDeviceToHost) != cudaSuccess || rec[0] == 0)
     return {};
-  char buf[160];
-  std::snprintf(buf, sizeof(buf), "cta %d waited on tile (%d, %d) for %d rows, saw %d", rec[1],
-                rec[2] / nt, rec[2] % nt, rec[3], rec[4]);
+  char buf[256];
+  std::snprintf(buf, sizeof(buf),
+                "cta %d waited on tile (%d, %d) for %d rows, saw %d (T %d; queue positions: "
+                "urgent %d of %d, bulk %d of %d)",
+                rec[1], rec[2] / nt, rec[2] % nt, rec[3], rec[4], w.T, rec[5], w.nurgent, rec[6],
+                w.ntasks - w.nurgent);
   return buf;
 }
 
@@ -2162,7 +2169,9 @@ cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long l
   }();
   const size_t tiles = static_cast<size_t>(nt) * nt * sizeof(int);
   cudaError_t e = cudaMemsetAsync(w.cnt, nodeps ? 0x3F : 0, tiles, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(w.cnt + static_cast<size_t>(nt) * nt, 0, w.cnt_bytes - tiles, s);
+  // queue positions and the abort flag; the watchdog record after them is
+  // kept across launches (zeroed at create): it names the first timeout
+  if (e == cudaSuccess) e = cudaMemsetAsync(w.cnt + static_cast<size_t>(nt) * nt, 0, 3 * sizeof(int), s);
   if (e != cudaSuccess) return e;
   Params prm;
   prm.a = a;
