@@ -99,6 +99,7 @@ struct Params {
   int pipe;       // GEMM tasks through gemm_pipe (TT_DAG_PIPE=0: the register path)
   int nodeps;     // TT_DAG_NODEPS=1 (measurement aid): every counter starts satisfied and
                   // no walker runs — the queues' task throughput alone, numerics void
+  int wide;       // bulk GEMM tasks with T <= 40 run 32-row strips (TT_DAG_WIDE=0: off)
   int pf_mask;    // bit 0: urgent CTAs, bit 1: bulk CTAs fetch the next task before
                   // the current one's dependency wait (else when warp 0 finishes it)
 };
@@ -659,9 +660,18 @@ __device__ void gemm_task(const Params& p, int j, int k0, int q, int r0, int r1,
 // groups retire in order.  The B tiles (q stacked, stage_b) are staged once
 // per task, their copies in flight together with each warp's first items.
 __host__ __device__ constexpr int sa_stride(int tp) { return tp % 16 == 8 ? tp : tp + 8; }
-__host__ __device__ constexpr int ring_slots(int nf) { return nf <= 5 ? 3 : 2; }
+// Ring slots per warp for strips of 8*smf rows.  Bulk GEMM tasks with T <= 40
+// run 32-row strips (smf = 4: twice the DMMAs per item, per poll and per
+// release, B fragments shared by four row blocks) in a 2-slot ring; the rest
+// 16-row strips in 3 (T <= 40) or 2 slots.
+__host__ __device__ constexpr int ring_slots(int nf, int smf = kMF) {
+  return smf == 4 ? 2 : (nf <= 5 ? 3 : 2);
+}
+__host__ __device__ constexpr bool wide_strips_ok(int nf) { return nf <= 5; }
 __host__ __device__ constexpr int ring_doubles(int nf) {
-  return kWarps * ring_slots(nf) * kStrip * sa_stride(nf * 8);
+  const int narrow = kWarps * ring_slots(nf, kMF) * kStrip * sa_stride(nf * 8);
+  const int wide = kWarps * ring_slots(nf, 4) * 32 * sa_stride(nf * 8);
+  return wide_strips_ok(nf) && wide > narrow ? wide : narrow;
 }
 // B tiles first (q stacked), the rings after them (16-byte aligned)
 __host__ __device__ constexpr int ring_offset(int q, int tp, bool chol) {
@@ -718,11 +728,12 @@ __device__ __forceinline__ void stage_b_async(const Params& p, double* Bs, int j
   cp_async_commit();
 }
 
-template <int NF, bool CHOL>
+template <int NF, bool CHOL, int SMF>
 __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
                           double* __restrict__ smem, bool eager, unsigned long long* first_done) {
-  constexpr int Tp = NF * 8, NPB = bstride(Tp, CHOL), SA = sa_stride(Tp), R = ring_slots(NF);
-  constexpr int HP = Tp / 2, kSlot = kStrip * SA;
+  constexpr int Tp = NF * 8, NPB = bstride(Tp, CHOL), SA = sa_stride(Tp), R = ring_slots(NF, SMF);
+  constexpr int GS = 8 * SMF;  // rows per strip
+  constexpr int HP = Tp / 2, kSlot = GS * SA;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
   const int T = p.T;
   const long long ld = p.ld;
@@ -730,7 +741,7 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
   const bool vec = !(T & 1);  // rows and tile origins 16-byte aligned (ld even, base aligned)
   const double* __restrict__ Bs = smem;
   double* ring = smem + ring_offset(q, Tp, CHOL) + warp * R * kSlot;
-  const int first = r0 + warp * kStrip, stride = kWarps * kStrip;
+  const int first = r0 + warp * GS, stride = kWarps * GS;
   const int ns = first < r1 ? (r1 - first + stride - 1) / stride : 0;
   const int per = q + 1;  // items per strip: q A steps, then C
   const int total = ns * per;
@@ -740,36 +751,36 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
   // vectors), the same for every item: vector v = lane + 32 u is row r_u,
   // column pair c_u; offsets precomputed once per task (the integer work of
   // the copy loop was 2-3 IMAD per DMMA).
-  constexpr int NVEC = (kStrip * HP + 31) / 32;
+  constexpr int NVEC = (GS * HP + 31) / 32;
   int goff[NVEC], soff[NVEC];
   unsigned rowmask = 0;  // bit u: vector u in a valid column; row checked per strip
   int vrow[NVEC];
 #pragma unroll
   for (int u = 0; u < NVEC; ++u) {
     const int e = lane + 32 * u, r = e / HP, c = 2 * (e - r * HP);
-    vrow[u] = e < kStrip * HP ? r : kStrip;
+    vrow[u] = e < GS * HP ? r : GS;
     goff[u] = r * static_cast<int>(ld) + c;
     soff[u] = r * SA + c;
-    if (e < kStrip * HP && c < T) rowmask |= 1u << u;
+    if (e < GS * HP && c < T) rowmask |= 1u << u;
   }
 
   int is_i = 0, is_kk = 0;  // strip / item of the next item to issue
   auto issue = [&](int y) {
     const int i = is_i, kk = is_kk;
-    const int ra = first + i * stride, nr = min(kStrip, r1 - ra);
+    const int ra = first + i * stride, nr = min(GS, r1 - ra);
     const double* src = p.a + static_cast<long long>(ra) * ld +
                         (kk < q ? static_cast<long long>(k0 + kk) * T : static_cast<long long>(jT));
     double* dst = ring + (y % R) * kSlot;
     if (vec) {
 #pragma unroll
       for (int u = 0; u < NVEC; ++u) {
-        if (vrow[u] < kStrip) {
+        if (vrow[u] < GS) {
           const bool valid = ((rowmask >> u) & 1) && vrow[u] < nr;
           cp_async16_zfill(dst + soff[u], valid ? src + goff[u] : p.a, valid);
         }
       }
     } else {  // odd T: synchronous copies (visible after the consumer's __syncwarp)
-      for (int e = lane; e < kStrip * Tp; e += 32) {
+      for (int e = lane; e < GS * Tp; e += 32) {
         const int r = e / Tp, c = e - r * Tp;
         dst[r * SA + c] = (r < nr && c < T) ? __ldcg(src + static_cast<long long>(r) * ld + c) : 0.0;
       }
@@ -783,7 +794,7 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
   unsigned a_ok = 0, c_ok = 0;
   {
     const int ti_lo = first / T;
-    const int ti_hi = ns > 0 ? (min(r1, first + (ns - 1) * stride + kStrip) - 1) / T : ti_lo - 1;
+    const int ti_hi = ns > 0 ? (min(r1, first + (ns - 1) * stride + GS) - 1) / T : ti_lo - 1;
     const int ntile = ti_hi - ti_lo + 1;
     bool tile_ok = false;  // lane d < ntile: tile row ti_lo + d, A dep; ntile <= d < 2 ntile: C dep
     if (ntile > 0 && 2 * ntile <= 32 && ns <= 32) {
@@ -797,7 +808,7 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
       const unsigned okm = __ballot_sync(0xffffffffu, tile_ok);
       const unsigned am = okm & ((1u << ntile) - 1), cm = (okm >> ntile) & ((1u << ntile) - 1);
       for (int i = 0; i < ns; ++i) {
-        const int rs = first + i * stride, re = min(r1, rs + kStrip);
+        const int rs = first + i * stride, re = min(r1, rs + GS);
         const int t0 = rs / T - ti_lo, t1 = (re - 1) / T - ti_lo;
         const unsigned need = ((2u << t1) - 1) & ~((1u << t0) - 1);
         if ((am & need) == need) a_ok |= 1u << i;
@@ -811,7 +822,7 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
     while (issued < total && issued < x + R) {
       const int y = issued, i = is_i, kk = is_kk;
       if ((kk == 0 && !((a_ok >> i) & 1)) || (kk == q && !((c_ok >> i) & 1))) {
-        const int rs = first + i * stride, re = min(r1, rs + kStrip);
+        const int rs = first + i * stride, re = min(r1, rs + GS);
         const bool blk = block_x && y == x;
         const bool ok = kk == 0 ? a_deps(p, rs, re, kl, blk) : strip_deps(p, rs, re, j, k0, -1, blk);
         if (!ok) {
@@ -834,9 +845,9 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
   __syncthreads();
   if (first_done && lane == 0) first_done[2] = globaltimer();
 
-  double acc[kMF][NF][2];
+  double acc[SMF][NF][2];
 #pragma unroll
-  for (int mf = 0; mf < kMF; ++mf)
+  for (int mf = 0; mf < SMF; ++mf)
 #pragma unroll
     for (int nf = 0; nf < NF; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
   int prev_ra = -1, prev_nr = 0;
@@ -845,28 +856,28 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
     cp_async_wait_n(issued - x - 1);
     __syncwarp();
     const double* slot = ring + (x % R) * kSlot;
-    const int ra = first + i * stride, nr = min(kStrip, r1 - ra);
+    const int ra = first + i * stride, nr = min(GS, r1 - ra);
     if (kk < q) {
       if (first_done && lane == 0 && x == 0) first_done[1] = globaltimer();
       const double* B = Bs + kk * Tp * NPB;
 #pragma unroll
       for (int s = 0; s < NF; ++s) {
         if (8 * s < T) {
-          double2 af[kMF];
+          double2 af[SMF];
 #pragma unroll
-          for (int mf = 0; mf < kMF; ++mf)
+          for (int mf = 0; mf < SMF; ++mf)
             af[mf] = *reinterpret_cast<const double2*>(slot + (mf * 8 + g) * SA + 8 * s + 2 * t);
           if (CHOL) {  // Bs[n][k]: both k-halves of lane t with one 16-byte load
             double2 bv[NF];
 #pragma unroll
             for (int nf = 0; nf < NF; ++nf)
               bv[nf] = *reinterpret_cast<const double2*>(B + (8 * nf + g) * NPB + 8 * s + 2 * t);
-            // k-half outer: consecutive DMMAs on one accumulator are kMF*NF
+            // k-half outer: consecutive DMMAs on one accumulator are SMF*NF
             // apart (back to back, the compiler pads the DMMA latency with NOPs)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
-              for (int mf = 0; mf < kMF; ++mf)
+              for (int mf = 0; mf < SMF; ++mf)
 #pragma unroll
                 for (int nf = 0; nf < NF; ++nf)
                   dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], h ? af[mf].y : af[mf].x,
@@ -878,7 +889,7 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
 #pragma unroll
               for (int nf = 0; nf < NF; ++nf) bv[nf] = B[(8 * s + 2 * t + h) * NPB + 8 * nf + g];
 #pragma unroll
-              for (int mf = 0; mf < kMF; ++mf)
+              for (int mf = 0; mf < SMF; ++mf)
 #pragma unroll
                 for (int nf = 0; nf < NF; ++nf)
                   dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], h ? af[mf].y : af[mf].x, bv[nf]);
@@ -894,7 +905,7 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
     } else {  // C item: C - sum, stores (Cholesky diagonal tiles: row >= col only)
       const int lower_off = CHOL ? ra - jT : kNoLower;
 #pragma unroll
-      for (int mf = 0; mf < kMF; ++mf) {
+      for (int mf = 0; mf < SMF; ++mf) {
         const int r = mf * 8 + g;
         if (r < nr) {
           double* crow = p.a + static_cast<long long>(ra + r) * ld + jT;
@@ -914,7 +925,7 @@ __device__ void gemm_pipe(const Params& p, int j, int k0, int q, int r0, int r1,
         }
       }
 #pragma unroll
-      for (int mf = 0; mf < kMF; ++mf)
+      for (int mf = 0; mf < SMF; ++mf)
 #pragma unroll
         for (int nf = 0; nf < NF; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
       if (first_done && lane == 0) {
@@ -1599,8 +1610,16 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
       // p.eager_sig: 0 none, 1 all GEMM tasks, 2 urgent-queue CTAs only, 3 bulk only
       const bool eager =
           p.eager_sig == 1 || (p.eager_sig == 2 && urgent_q) || (p.eager_sig == 3 && !urgent_q);
-      gemm_pipe<NF, CHOL>(p, j, k, task_q(tk), r0, r1, sm, eager,
-                          (p.trace && warp == 0) ? &s_ph[1] : nullptr);
+      // 32-row strips for large bulk-queue tasks (T <= 40, >= 512 rows: two
+      // strips per warp; NODEPS 1.35 -> 1.24 ms on Cholesky XL); the urgent
+      // band and smaller tasks keep 16-row strips (finer dataflow: LU N=2000
+      // with 400-row tasks measured 3% slower on 32-row strips)
+      if (wide_strips_ok(NF) && p.wide && !urgent_q && r1 - r0 >= 512)
+        gemm_pipe<NF, CHOL, (wide_strips_ok(NF) ? 4 : kMF)>(p, j, k, task_q(tk), r0, r1, sm, eager,
+                                                        (p.trace && warp == 0) ? &s_ph[1] : nullptr);
+      else
+        gemm_pipe<NF, CHOL, kMF>(p, j, k, task_q(tk), r0, r1, sm, eager,
+                                 (p.trace && warp == 0) ? &s_ph[1] : nullptr);
     } else if (kind == kGemm && task_q(tk) > 1) {  // chunked: q steps, K = q*T
       const int q = task_q(tk);
       stage_b<NF, CHOL>(p, sm, j, k, q);
@@ -2193,6 +2212,10 @@ cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long l
   prm.fence = [] {
     const char* v = std::getenv("TT_DAG_FENCE");
     return v && v[0] == '1' ? 1 : 0;
+  }();
+  prm.wide = [] {
+    const char* v = std::getenv("TT_DAG_WIDE");
+    return v && v[0] == '0' ? 0 : 1;
   }();
   prm.pipe = w.pipe;  // fixed at create(): the chunk depth's shared-memory budget depends on it
   prm.d = w.chunk;

@@ -398,6 +398,7 @@ class BayesOptTuner final : public Tuner {
     for (auto f : hist_flat_) X.push_back(encode(space_, config_at(space_, f)));
     const Forest model = fit_forest(X, log_runtimes_, 25, 12, 2, seed_);
     std::vector<std::pair<double, std::uint64_t>> scored(pool.size());
+    std::vector<std::pair<double, double>> pred(pool.size());  // (mean, sd) per candidate
     const int np = static_cast<int>(pool.size());
     const int chunks = std::min(host_threads(), std::max(1, np / 256));
     parallel_for(chunks, chunks, [&](int c) {
@@ -406,6 +407,7 @@ class BayesOptTuner final : public Tuner {
         double m, sd;
         predict_forest(model, e.data(), &m, &sd);
         scored[i] = {m - 1.96 * sd, pool[i]};  // lcb, kappa = 1.96 (tuners.hpp:172-176)
+        pred[i] = {m, sd};
       }
     });
     if (need == 1) {  // first strict minimum over the ascending pool
@@ -414,10 +416,31 @@ class BayesOptTuner final : public Tuner {
         if (p.first < best.first) best = p;
       out.push_back(best.second);
     } else {
-      std::stable_sort(scored.begin(), scored.end(),
-                       [](const auto& a, const auto& b) { return a.first < b.first; });
-      for (int i = 0; i < need && i < static_cast<int>(scored.size()); ++i)
+      // k best LCB scores, one per model cell first: candidates whose (mean,
+      // sd) equals an already chosen one's fall in the same leaf of every
+      // tree — the forest cannot tell them apart, so a batch of them would
+      // spend k evaluations on one prediction.  Cells are skipped until each
+      // chosen candidate is from a distinct cell, then the batch is filled in
+      // score order.
+      std::vector<int> order(np);
+      for (int i = 0; i < np; ++i) order[i] = i;
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int a, int b) { return scored[a].first < scored[b].first; });
+      std::vector<std::pair<double, double>> cells;
+      std::vector<int> skipped;
+      for (int i : order) {
+        if (static_cast<int>(out.size()) == need) break;
+        if (std::find(cells.begin(), cells.end(), pred[i]) != cells.end()) {
+          skipped.push_back(i);
+          continue;
+        }
+        cells.push_back(pred[i]);
         out.push_back(scored[i].second);
+      }
+      for (int i : skipped) {
+        if (static_cast<int>(out.size()) == need) break;
+        out.push_back(scored[i].second);
+      }
     }
     return out;
   }

@@ -19,7 +19,14 @@ ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--warmup", type=int, default=1)
 ap.add_argument("--kblocks", type=int, default=8)
 a = ap.parse_args()
-out = run_scaled(a.n, a.steps, a.warmup, a.kblocks)
+import os  # noqa: E402
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from bench import ClockSampler  # noqa: E402
+
+# SM clock + throttle reasons sampled over the whole run (the timed steps dominate it)
+with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+    out = run_scaled(a.n, a.steps, a.warmup, a.kblocks)
 if out is not None:
+    out["clocks"] = clk.summary()
     out["pct_of_fp64_peak_per_gpu"] = 100.0 * out["tflops"] / out["world"] / 37.05
     print(json.dumps(out), flush=True)
