@@ -49,8 +49,9 @@ constexpr int kABuf = kStrip * kAW;              // doubles per buffer
 constexpr int kSmemA = kWarps * 2 * kABuf;       // all warps' A buffers
 // walker-only: DIAG block inverses (1024) + the U12-solve block inverses (512)
 constexpr int kSmemW = 1536;
-// walker: tiles D, L(k+1,k), U(k,k+1), the reciprocals rk (128) and the inverses
-constexpr int kWalkerSmem = 3 * kSmemB + 128 + kSmemW;
+// walker: tiles D, L(k+1,k), U(k,k+1), the reciprocals rk (128), the inverses
+// and the prefetch buffer of the next diagonal tile
+constexpr int kWalkerSmem = 4 * kSmemB + 128 + kSmemW;
 // Dynamic shared memory of every CTA (one CTA per SM): the walker's tiles, a
 // queue CTA's TRSM tile + block inverses, or a GEMM task's q stacked B tiles.
 constexpr int kSmemBytes = 224 * 1024;
@@ -1042,6 +1043,19 @@ __device__ __forceinline__ void tile_load(double* D, const double* __restrict__ 
   }
 }
 
+// tile_load from the raw rows in shared memory (the walker's prefetch buffer P):
+// Cholesky mirrors the lower triangle, identity padding outside T x T.
+template <bool CHOL>
+__device__ __forceinline__ void tile_from_raw(double* D, const double* P, int T) {
+  constexpr int kPer = 64 * 64 / kThreads;
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = threadIdx.x + u * kThreads, i = e >> 6, c = e & 63;
+    const int si = (CHOL && c > i) ? c : i, sc = (CHOL && c > i) ? i : c;
+    D[i * kNP + c] = (i < T && c < T) ? P[si * kNP + sc] : (i == c ? 1.0 : 0.0);
+  }
+}
+
 // 8x8 diagonal block b (one warp, fragment layout, shuffles) + inv(U_bb),
 // inv(L_bb).  Called by warp 0 only.
 template <bool CHOL>
@@ -1359,10 +1373,12 @@ __device__ void walker(const Params& p, double* dsm) {
   double* rk = Ut + kSmemB;                 // 128
   double* inv = rk + 128;                   // 1024: DIAG block inverses
   double* invX = inv + 1024;                // 512: inverses for the second solve
+  double* P = invX + 512;                   // prefetched tile (k+1,k+1), raw rows
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int T = p.T, nt = p.nt;
   const long long ld = p.ld;
-  __shared__ int s_ok;
+  __shared__ int s_ok, s_pf, s_pl, s_pu;
+  bool pref = false;  // tile (k,k) of this step was prefetched into P (stages < k-1)
   auto wait1 = [&](const int* c, int need) -> bool {  // whole CTA
     if (tid == 0) s_ok = wait_ge(p, c, need);
     __syncthreads();
@@ -1378,9 +1394,16 @@ __device__ void walker(const Params& p, double* dsm) {
     stamp(k, 0);
     // the updates of steps < k-1 of tile (k,k) come from the queue's GEMM
     // tasks (step k-1 is always a single step: the walker applies it)
-    if (k >= 2 && !wait1(&p.cnt[k * nt + k], need_before(p, k, k, k - 1))) return;
-    stamp(k, 1);
-    tile_load<CHOL>(D, dk, ld, T);
+    if (pref) {  // copies issued during the previous step's panel solves
+      cp_async_wait<0>();
+      __syncthreads();
+      stamp(k, 1);
+      tile_from_raw<CHOL>(D, P, T);
+    } else {
+      if (k >= 2 && !wait1(&p.cnt[k * nt + k], need_before(p, k, k, k - 1))) return;
+      stamp(k, 1);
+      tile_load<CHOL>(D, dk, ld, T);
+    }
     __syncthreads();
     if (k >= 1) {  // stage k-1: D -= L(k,k-1) * U(k-1,k) (Cholesky: L L^T), DMMA in smem
       if (8 * warp < Tp) {
@@ -1414,11 +1437,45 @@ __device__ void walker(const Params& p, double* dsm) {
     stamp(k, 2);
     diag_blocked<CHOL>(D, T, kT, p.info, inv, rk);
     stamp(k, 3);
+    // Polls next to the tile store (warps 1-3, one lane each): the panel inputs
+    // A(k+1,k) (and A(k,k+1)) at stage k-1, and the next diagonal tile at
+    // stage k-1 (the walker applies stage k itself).  What is already final is
+    // copied into shared memory (cp.async, warps 1-7) while thread 0's release
+    // of DIAG(k) drains, instead of a poll and a load round trip after it.
+    const bool more = k + 1 < nt;
+    if (more && tid == 32)
+      s_pf = !(T & 1) && ld_acquire(&p.cnt[(k + 1) * nt + k + 1]) >= need_before(p, k + 1, k + 1, k);
+    if (more && tid == 64)
+      s_pl = T == Tp && !(T & 1) && ld_acquire(&p.cnt[(k + 1) * nt + k]) >= need_before(p, k, k, k);
+    if (more && tid == 96)
+      s_pu = CHOL || (T == Tp && !(T & 1) &&
+                      ld_acquire(&p.cnt[k * nt + k + 1]) >= need_before(p, k, k + 1, k));
     tile_store<CHOL>(D, dk, ld, T, rk, p.solve + static_cast<long long>(k) * kSolveSlot);
     // publish: the CTA barrier orders every thread's stores before thread 0's
     // release reduction (cumulative), so one fence instead of one per warp.
     // Only warp 0 records failures (factor_block8), so thread 0 sees them.
     __syncthreads();
+    const bool pan = more && s_pl && s_pu;
+    pref = more && s_pf;
+    if (warp > 0 && (pan || pref)) {  // (warp 0 issues none: thread 0's fence below)
+      const int hp = T >> 1, t7 = tid - 32;
+      if (pan) {
+        const double* al = p.a + static_cast<long long>(kT + T) * ld + kT;
+        for (int e = t7; e < T * hp; e += kThreads - 32) {
+          const int i = e / hp, c = 2 * (e - i * hp);
+          cp_async16(Lt + i * kNP + c, al + static_cast<long long>(i) * ld + c);
+          if (!CHOL) cp_async16(Ut + i * kNP + c, dk + T + static_cast<long long>(i) * ld + c);
+        }
+      }
+      if (pref) {
+        const double* dn = dk + static_cast<long long>(T) * ld + T;
+        for (int e = t7; e < T * hp; e += kThreads - 32) {
+          const int i = e / hp, c = 2 * (e - i * hp);
+          cp_async16(P + i * kNP + c, dn + static_cast<long long>(i) * ld + c);
+        }
+      }
+      cp_async_commit();
+    }
     if (tid == 0) {
       const bool f = diag::failed(p.info);
       s_ok = !f;
@@ -1429,8 +1486,17 @@ __device__ void walker(const Params& p, double* dsm) {
     }
     __syncthreads();
     if (!s_ok) return;
-    if (k + 1 >= nt) break;
+    if (!more) break;
     // ---- first tiles of the panel: L(k+1,k) = A(k+1,k) U11^-1, U(k,k+1) = L11^-1 A(k,k+1)
+    if (pan) {
+      cp_async_wait<0>();
+      stamp(k, 4);
+      for (int e = tid; e < NF * 64; e += kThreads) {  // inverses for the second solve (below)
+        const int b = e >> 6, ii = (e >> 3) & 7, c = e & 7;
+        const double v = inv[512 + b * 64 + c * 8 + ii];
+        invX[e] = CHOL ? v * (8 * b + c < T ? rk[8 * b + c] : 1.0) : v;
+      }
+    } else {
     if (!wait1(&p.cnt[(k + 1) * nt + k], need_before(p, k, k, k))) return;
     if (!CHOL && !wait1(&p.cnt[k * nt + k + 1], need_before(p, k, k + 1, k))) return;
     stamp(k, 4);
@@ -1477,6 +1543,7 @@ __device__ void walker(const Params& p, double* dsm) {
         }
       }
     }
+    }  // panel not prefetched
     __syncthreads();
     stamp(k, 6);
     // warps 0..3: L21 strips (X * M = A21); warps 4..7: U12 strips on the
