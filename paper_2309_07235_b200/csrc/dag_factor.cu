@@ -142,7 +142,12 @@ __device__ bool wait_ge(const Params& p, const int* addr, int need) {
       if (ld_acquire(addr) >= need) break;
       if ((it & 15) == 15) {
         if (ld_relaxed(p.abort)) return false;
-        if (globaltimer() - t0 > static_cast<unsigned long long>(kWatchdogNs)) {
+        // timeout = 4 s of %globaltimer AND >= 2^20 polls (each >= 100 ns of
+        // sleep), so one anomalous timer reading cannot abort a healthy
+        // schedule (long sweeps once reported a timeout whose record showed
+        // no progress at all)
+        const long long dt = static_cast<long long>(globaltimer() - t0);
+        if (it >= (1 << 20) && dt > kWatchdogNs) {
           // first expiring waiter records what it waited for (diagnostics:
           // CTA, counter index, target, last value seen)
           if (atomicCAS(p.abort + 2, 0, 1) == 0) {
@@ -152,6 +157,8 @@ __device__ bool wait_ge(const Params& p, const int* addr, int need) {
             p.abort[6] = ld_relaxed(addr);
             p.abort[7] = ld_relaxed(p.next);      // urgent queue position
             p.abort[8] = ld_relaxed(p.next + 2);  // bulk queue position
+            p.abort[9] = it;                          // polls
+            p.abort[10] = static_cast<int>(dt / 1000000);  // ms waited
           }
           atomicExch(p.abort, 2);
           atomicMin(p.info, kTimeout);
@@ -2190,7 +2197,8 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   w->pipe = pipe_gemm() ? 1 : 0;
   w->nsteps = nt;
   // nt*nt tile counters, then: urgent next, abort flag, bulk next, and the
-  // watchdog record {recorded, cta, counter, need, seen, urgent pos, bulk pos} (kDiagInts)
+  // watchdog record {recorded, cta, counter, need, seen, urgent pos, bulk pos, polls, ms}
+  // (kDiagInts)
   w->cnt_bytes = (static_cast<size_t>(nt) * nt + 3 + kDiagInts) * sizeof(int);
   cudaError_t e = cudaMalloc(&w->tasks, tasks.size() * sizeof(int4));
   if (e != cudaSuccess) return e;
@@ -2232,9 +2240,9 @@ std::string watchdog_info(const Workspace& w) {
   char buf[256];
   std::snprintf(buf, sizeof(buf),
                 "cta %d waited on tile (%d, %d) for %d rows, saw %d (T %d; queue positions: "
-                "urgent %d of %d, bulk %d of %d)",
+                "urgent %d of %d, bulk %d of %d; %d polls, %d ms)",
                 rec[1], rec[2] / nt, rec[2] % nt, rec[3], rec[4], w.T, rec[5], w.nurgent, rec[6],
-                w.ntasks - w.nurgent);
+                w.ntasks - w.nurgent, rec[7], rec[8]);
   return buf;
 }
 
