@@ -1067,7 +1067,7 @@ __device__ __forceinline__ void tile_from_raw(double* D, const double* P, int T)
 // inv(L_bb).  Called by warp 0 only.
 template <bool CHOL>
 __device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* info, double* inv,
-                                              double* rk, int b) {
+                                              double* rk, int b, int* sfail) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int p = 8 * b;
   double* invU = inv + b * 64;
@@ -1107,7 +1107,10 @@ __device__ __forceinline__ void factor_block8(double* D, int T, int gcol, int* i
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk)
     if (p + kk < T) rk[p + kk] = rr[kk];  // same value from every lane
-  if (fail != INT_MAX && lane == 0) atomicMin(info, gcol + p + fail);
+  if (fail != INT_MAX && lane == 0) {
+    atomicMin(info, gcol + p + fail);
+    *sfail = 1;  // the walker checks this shared flag, not the global status word
+  }
   __syncwarp();
   // inv(U_bb) (lanes 0..7) and inv(L_bb) (lanes 8..15), one column per lane,
   // by back substitution without divisions.  Both run the same instruction
@@ -1178,10 +1181,10 @@ __device__ __forceinline__ void trail_row(double* D, int b, int nr, int ir, int 
 // overlaps the bulk of step b.  Two __syncthreads per 8 pivots.
 template <bool CHOL>
 __device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* info, double* inv,
-                                             double* rk) {
+                                             double* rk, int* sfail) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int NB = (T + 7) >> 3;
-  if (warp == 0) factor_block8<CHOL>(D, T, gcol, info, inv, rk, 0);
+  if (warp == 0) factor_block8<CHOL>(D, T, gcol, info, inv, rk, 0, sfail);
   __syncthreads();
   for (int b = 0; b + 1 < NB; ++b) {
     const int p = 8 * b, nr = NB - b - 1;
@@ -1215,7 +1218,7 @@ __device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* in
     if (warp == 0) {  // look-ahead: diagonal block (b+1,b+1) first, then factor it
       trail_row(D, b, 1, 0, 0);
       __syncwarp();
-      factor_block8<CHOL>(D, T, gcol, info, inv, rk, b + 1);
+      factor_block8<CHOL>(D, T, gcol, info, inv, rk, b + 1, sfail);
     } else {  // the rest of step b's trailing update
       // warps 1-3, 5-7 only: warp 4 shares warp 0's SM sub-partition; keeping
       // its DMMAs off it measured a slightly shorter DIAG (9.8 vs 10.1 us/step)
@@ -1384,7 +1387,8 @@ __device__ void walker(const Params& p, double* dsm) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int T = p.T, nt = p.nt;
   const long long ld = p.ld;
-  __shared__ int s_ok, s_pf, s_pl, s_pu;
+  __shared__ int s_ok, s_pf, s_pl, s_pu, s_fail;
+  if (tid == 0) s_fail = 0;  // (visible after the first barrier below)
   bool pref = false;  // tile (k,k) of this step was prefetched into P (stages < k-1)
   auto wait1 = [&](const int* c, int need) -> bool {  // whole CTA
     if (tid == 0) s_ok = wait_ge(p, c, need);
@@ -1442,7 +1446,7 @@ __device__ void walker(const Params& p, double* dsm) {
       __syncthreads();
     }
     stamp(k, 2);
-    diag_blocked<CHOL>(D, T, kT, p.info, inv, rk);
+    diag_blocked<CHOL>(D, T, kT, p.info, inv, rk, &s_fail);
     stamp(k, 3);
     // Polls next to the tile store (warps 1-3, one lane each): the panel inputs
     // A(k+1,k) (and A(k,k+1)) at stage k-1, and the next diagonal tile at
@@ -1460,7 +1464,8 @@ __device__ void walker(const Params& p, double* dsm) {
     tile_store<CHOL>(D, dk, ld, T, rk, p.solve + static_cast<long long>(k) * kSolveSlot);
     // publish: the CTA barrier orders every thread's stores before thread 0's
     // release reduction (cumulative), so one fence instead of one per warp.
-    // Only warp 0 records failures (factor_block8), so thread 0 sees them.
+    // A failing pivot (factor_block8, warp 0) raised s_fail before DIAG's last
+    // barrier: no global read of the status word on the chain.
     __syncthreads();
     const bool pan = more && s_pl && s_pu;
     pref = more && s_pf;
@@ -1484,7 +1489,7 @@ __device__ void walker(const Params& p, double* dsm) {
       cp_async_commit();
     }
     if (tid == 0) {
-      const bool f = diag::failed(p.info);
+      const bool f = s_fail != 0;
       s_ok = !f;
       if (f)
         atomicExch(p.abort, 1);
