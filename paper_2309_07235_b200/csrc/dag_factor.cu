@@ -1001,16 +1001,16 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // :297-302; NaN passes).
 // inv: [b*64, +64) inv(U_bb) row-major, [512 + b*64, +64) inv(L_bb) row-major.
 // rk[c] = 1/u_cc.
-template <bool CHOL>
+template <bool CHOL, int NTH = kThreads>
 __device__ __forceinline__ void tile_load(double* D, const double* __restrict__ dk, long long ld,
                                           int T) {
   if (!(T & 1)) {  // element pairs (16-byte loads); Cholesky mirrors the lower triangle
-    constexpr int kPer = 64 * 32 / kThreads;
+    constexpr int kPer = (64 * 32 + NTH - 1) / NTH;
     double2 v[kPer];
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
-      const int e = threadIdx.x + u * kThreads, i = e >> 5, c = 2 * (e & 31);
-      if (i < T && c < T && (!CHOL || c <= i))
+      const int e = threadIdx.x + u * NTH, i = e >> 5, c = 2 * (e & 31);
+      if (e < 64 * 32 && i < T && c < T && (!CHOL || c <= i))
         v[u] = __ldcg(reinterpret_cast<const double2*>(dk + static_cast<long long>(i) * ld + c));
       else
         v[u] = make_double2(i == c ? 1.0 : 0.0, i == c + 1 ? 1.0 : 0.0);
@@ -1018,7 +1018,8 @@ __device__ __forceinline__ void tile_load(double* D, const double* __restrict__ 
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
-      const int e = threadIdx.x + u * kThreads, i = e >> 5, c = 2 * (e & 31);
+      const int e = threadIdx.x + u * NTH, i = e >> 5, c = 2 * (e & 31);
+      if (e >= 64 * 32) break;
       if (!CHOL) {
         *reinterpret_cast<double2*>(D + i * kNP + c) = v[u];
       } else {
@@ -1034,30 +1035,28 @@ __device__ __forceinline__ void tile_load(double* D, const double* __restrict__ 
     }
     return;
   }
-  constexpr int kPer = 64 * 64 / kThreads;
+  constexpr int kPer = (64 * 64 + NTH - 1) / NTH;
   double v[kPer];
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {  // Cholesky: mirror the lower triangle
-    const int e = threadIdx.x + u * kThreads, i = e >> 6, c = e & 63;
+    const int e = threadIdx.x + u * NTH, i = e >> 6, c = e & 63;
     const int si = (CHOL && c > i) ? c : i, sc = (CHOL && c > i) ? i : c;
-    v[u] = (i < T && c < T) ? __ldcg(dk + static_cast<long long>(si) * ld + sc)
-                            : (i == c ? 1.0 : 0.0);
+    v[u] = (e < 4096 && i < T && c < T) ? __ldcg(dk + static_cast<long long>(si) * ld + sc)
+                                        : (i == c ? 1.0 : 0.0);
   }
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
-    const int e = threadIdx.x + u * kThreads;
-    D[(e >> 6) * kNP + (e & 63)] = v[u];
+    const int e = threadIdx.x + u * NTH;
+    if (e < 4096) D[(e >> 6) * kNP + (e & 63)] = v[u];
   }
 }
 
 // tile_load from the raw rows in shared memory (the walker's prefetch buffer P):
 // Cholesky mirrors the lower triangle, identity padding outside T x T.
-template <bool CHOL>
+template <bool CHOL, int NTH = kThreads>
 __device__ __forceinline__ void tile_from_raw(double* D, const double* P, int T) {
-  constexpr int kPer = 64 * 64 / kThreads;
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const int e = threadIdx.x + u * kThreads, i = e >> 6, c = e & 63;
+  for (int e = threadIdx.x; e < 4096; e += NTH) {
+    const int i = e >> 6, c = e & 63;
     const int si = (CHOL && c > i) ? c : i, sc = (CHOL && c > i) ? i : c;
     D[i * kNP + c] = (i < T && c < T) ? P[si * kNP + sc] : (i == c ? 1.0 : 0.0);
   }
@@ -1175,24 +1174,34 @@ __device__ __forceinline__ void trail_row(double* D, int b, int nr, int ir, int 
   }
 }
 
+// Barrier over the first NW warps of the CTA (all 8: __syncthreads; fewer:
+// named barrier 1 — the walker's compute warps while warp 7 publishes).
+template <int NW>
+__device__ __forceinline__ void csync() {
+  if (NW == kWarps)
+    __syncthreads();
+  else
+    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+}
+
 // Blocked elimination of the tile in shared memory with look-ahead: while
 // warps 1..7 apply step b's trailing update, warp 0 updates the next
 // diagonal block first and factors it, so the serial 8x8 chain of block b+1
 // overlaps the bulk of step b.  Two __syncthreads per 8 pivots.
-template <bool CHOL>
+template <bool CHOL, int NW = kWarps>
 __device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* info, double* inv,
                                              double* rk, int* sfail) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int NB = (T + 7) >> 3;
   if (warp == 0) factor_block8<CHOL>(D, T, gcol, info, inv, rk, 0, sfail);
-  __syncthreads();
+  csync<NW>();
   for (int b = 0; b + 1 < NB; ++b) {
     const int p = 8 * b, nr = NB - b - 1;
     const double* invU = inv + b * 64;
     const double* invL = inv + 512 + b * 64;
     // ---- panels: job < nr: L block (b+1+job, b) = A * inv(U_bb);
     //               job >= nr: U block (b, b+1+job-nr) = inv(L_bb) * A
-    for (int job = warp; job < 2 * nr; job += kWarps) {
+    for (int job = warp; job < 2 * nr; job += NW) {
       double c0 = 0.0, c1 = 0.0;
       if (job < nr) {
         const int rb = 8 * (b + 1 + job);
@@ -1214,7 +1223,7 @@ __device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* in
         D[(p + g) * kNP + cb + 2 * t + 1] = c1;
       }
     }
-    __syncthreads();
+    csync<NW>();
     if (warp == 0) {  // look-ahead: diagonal block (b+1,b+1) first, then factor it
       trail_row(D, b, 1, 0, 0);
       __syncwarp();
@@ -1224,10 +1233,10 @@ __device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* in
       // its DMMAs off it measured a slightly shorter DIAG (9.8 vs 10.1 us/step)
       if (warp != 4) {
         const int wi = warp < 4 ? warp - 1 : warp - 2;
-        for (int ir = wi; ir < nr; ir += kWarps - 2) trail_row(D, b, nr, ir, ir == 0 ? 1 : 0);
+        for (int ir = wi; ir < nr; ir += NW - 2) trail_row(D, b, nr, ir, ir == 0 ? 1 : 0);
       }
     }
-    __syncthreads();
+    csync<NW>();
   }
   // Cholesky: l_jj = sqrt(u_jj) (rk[64 + j]) and 1/l_jj (rk[j]) for the solves
   if (CHOL && tid < T) {
@@ -1235,18 +1244,16 @@ __device__ __forceinline__ void diag_blocked(double* D, int T, int gcol, int* in
     rk[64 + tid] = l;
     rk[tid] = rcp_nr(l);
   }
-  __syncthreads();
+  csync<NW>();
 }
 
 // Factored tile -> global (Cholesky: lower only, scaled) and the diagonal
 // reciprocals -> the step's solve slot (read by the TRSM tasks).
-template <bool CHOL>
+template <bool CHOL, int NTH = kThreads>
 __device__ __forceinline__ void tile_store(const double* D, double* __restrict__ dk, long long ld,
                                            int T, const double* rk, double* solve) {
-  constexpr int kPer = 64 * 64 / kThreads;
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const int e = threadIdx.x + u * kThreads, i = e >> 6, c = e & 63;
+  for (int e = threadIdx.x; e < 64 * 64; e += NTH) {
+    const int i = e >> 6, c = e & 63;
     if (i < T && c < T && (!CHOL || c <= i)) {
       double v = D[i * kNP + c];
       if (CHOL) v = c == i ? rk[64 + c] : v * rk[64 + c];
@@ -1368,12 +1375,44 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
 }
 
 // ---------------------------------------------------------------- walker
-// CTA 0 walks the diagonal: per panel step k it applies the step-(k-1)
-// update to tile (k,k) with the L and U tiles it solved itself, factors the
-// tile, and solves the first tiles of the panel (L(k+1,k), U(k,k+1)), all in
-// shared memory — the latency-critical chain DIAG(k) -> TRSM -> GEMM ->
-// DIAG(k+1) never leaves the SM.  The other CTAs run the bulk TRSM/GEMM tasks
-// from the queue; the walker publishes its tiles with the same counters.
+// The walker's publisher warp (tiles <= 48, see walker): the compute warps
+// store the factored diagonal tile and the solved panel tiles themselves (224
+// threads, no waiting), hand over at a barrier + shared step counter, and
+// lane 0 of warp 7 issues the release reductions — whose fence waits for
+// those stores to reach L2 (~1 us) — off the chain.  Cumulativity: the
+// stores precede the compute warps' barrier, thread 0's flag write (after a
+// CTA fence) and this warp's flag read (before a CTA fence), so the
+// gpu-scope release covers them, as it covers a CTA's stores after a
+// __syncthreads in warp_signal's pattern.
+// Returns when the compute warps stop (wabort), a pivot failed (raises the
+// schedule's abort flag), or after the last step.
+template <int NF, bool CHOL>
+__device__ void walker_publisher(const Params& p, const int* sfail, volatile int* dready,
+                                 volatile int* luready, volatile int* wabort) {
+  if ((threadIdx.x & 31) != 0) return;
+  const int T = p.T, nt = p.nt;
+  auto await = [&](volatile int* f, int k) -> bool {
+    while (*f < k) {
+      if (*wabort) return false;
+      __nanosleep(32);
+    }
+    __threadfence_block();
+    return true;
+  };
+  for (int k = 0; k < nt; ++k) {
+    if (!await(dready, k)) return;
+    if (*reinterpret_cast<const volatile int*>(sfail)) {
+      atomicExch(p.abort, 1);
+      return;
+    }
+    red_release_add(&p.cnt[k * nt + k], k >= 1 ? 2 * T : T);  // stage k-1 + DIAG(k)
+    if (k + 1 >= nt) return;
+    if (!await(luready, k)) return;
+    red_release_add(&p.cnt[(k + 1) * nt + k], T);
+    if (!CHOL) red_release_add(&p.cnt[k * nt + k + 1], T);
+  }
+}
+
 template <int NF, bool CHOL>
 __device__ void walker(const Params& p, double* dsm) {
   constexpr int Tp = NF * 8;
@@ -1387,12 +1426,31 @@ __device__ void walker(const Params& p, double* dsm) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int T = p.T, nt = p.nt;
   const long long ld = p.ld;
-  __shared__ int s_ok, s_pf, s_pl, s_pu, s_fail;
-  if (tid == 0) s_fail = 0;  // (visible after the first barrier below)
+  // PUB (Cholesky, tiles <= 48): warp 7 is the walker's publisher — it releases the
+  // counters of the tiles the compute warps 0-6 stored (walker_publisher), so
+  // the release fences (~1 us each, two per step) leave the chain.
+  constexpr bool PUB = CHOL && NF <= 6;  // measured: Cholesky XL -1%, LU +3% (7 compute warps)
+  constexpr int NW = PUB ? kWarps - 1 : kWarps;  // compute warps
+  constexpr int NC = NW * 32;
+  __shared__ int s_ok, s_pf, s_pl, s_pu, s_fail, s_el, s_eu;
+  __shared__ volatile int s_dready, s_luready, s_wabort;
+  if (tid == 0) {
+    s_fail = 0;
+    s_dready = s_luready = -1;
+    s_wabort = 0;
+  }
+  __syncthreads();
+  if (PUB && warp == kWarps - 1) {
+    walker_publisher<NF, CHOL>(p, &s_fail, &s_dready, &s_luready, &s_wabort);
+    return;
+  }
   bool pref = false;  // tile (k,k) of this step was prefetched into P (stages < k-1)
-  auto wait1 = [&](const int* c, int need) -> bool {  // whole CTA
-    if (tid == 0) s_ok = wait_ge(p, c, need);
-    __syncthreads();
+  auto wait1 = [&](const int* c, int need) -> bool {  // compute warps
+    if (tid == 0) {
+      s_ok = wait_ge(p, c, need);
+      if (!s_ok) s_wabort = 1;  // the publisher stops too
+    }
+    csync<NW>();
     return s_ok;
   };
   auto stamp = [&](int k, int i) {
@@ -1407,15 +1465,15 @@ __device__ void walker(const Params& p, double* dsm) {
     // tasks (step k-1 is always a single step: the walker applies it)
     if (pref) {  // copies issued during the previous step's panel solves
       cp_async_wait<0>();
-      __syncthreads();
+      csync<NW>();
       stamp(k, 1);
-      tile_from_raw<CHOL>(D, P, T);
+      tile_from_raw<CHOL, NC>(D, P, T);
     } else {
       if (k >= 2 && !wait1(&p.cnt[k * nt + k], need_before(p, k, k, k - 1))) return;
       stamp(k, 1);
-      tile_load<CHOL>(D, dk, ld, T);
+      tile_load<CHOL, NC>(D, dk, ld, T);
     }
-    __syncthreads();
+    csync<NW>();
     if (k >= 1) {  // stage k-1: D -= L(k,k-1) * U(k-1,k) (Cholesky: L L^T), DMMA in smem
       if (8 * warp < Tp) {
         const int r = 8 * warp;
@@ -1443,10 +1501,37 @@ __device__ void walker(const Params& p, double* dsm) {
           D[(r + g) * kNP + nf * 8 + 2 * t + 1] = acc[nf][1];
         }
       }
-      __syncthreads();
+      csync<NW>();
+    }
+    // Early panel copy (PUB): if the panel inputs A(k+1,k) (and A(k,k+1)) are
+    // final already, warp 2 (and warp 3) copy them into Lt (Ut) now, under
+    // DIAG(k) (step k-1's panel tiles were stored before the step began).
+    const bool try_early = PUB && k + 1 < nt && T == Tp && !(T & 1);
+    if (try_early && (warp == 2 || (!CHOL && warp == 3))) {
+      const bool lo = warp == 2;
+      int ok = 0;
+      if (lane == 0)
+        ok = lo ? ld_acquire(&p.cnt[(k + 1) * nt + k]) >= need_before(p, k, k, k)
+                : ld_acquire(&p.cnt[k * nt + k + 1]) >= need_before(p, k, k + 1, k);
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (ok) {
+        const int hp = T >> 1;
+        const double* src = lo ? p.a + static_cast<long long>(kT + T) * ld + kT : dk + T;
+        double* dst = lo ? Lt : Ut;
+        for (int e = lane; e < T * hp; e += 32) {
+          const int i = e / hp, c = 2 * (e - i * hp);
+          cp_async16(dst + i * kNP + c, src + static_cast<long long>(i) * ld + c);
+        }
+        cp_async_commit();
+      }
+      if (lane == 0) {
+        if (lo) s_el = ok;
+        else s_eu = ok;
+      }
     }
     stamp(k, 2);
-    diag_blocked<CHOL>(D, T, kT, p.info, inv, rk, &s_fail);
+    diag_blocked<CHOL, NW>(D, T, kT, p.info, inv, rk, &s_fail);
+    const bool epan = try_early && s_el && (CHOL || s_eu);  // (after DIAG's barriers)
     stamp(k, 3);
     // Polls next to the tile store (warps 1-3, one lane each): the panel inputs
     // A(k+1,k) (and A(k,k+1)) at stage k-1, and the next diagonal tile at
@@ -1456,24 +1541,31 @@ __device__ void walker(const Params& p, double* dsm) {
     const bool more = k + 1 < nt;
     if (more && tid == 32)
       s_pf = !(T & 1) && ld_acquire(&p.cnt[(k + 1) * nt + k + 1]) >= need_before(p, k + 1, k + 1, k);
-    if (more && tid == 64)
+    if (more && !epan && tid == 64)
       s_pl = T == Tp && !(T & 1) && ld_acquire(&p.cnt[(k + 1) * nt + k]) >= need_before(p, k, k, k);
-    if (more && tid == 96)
+    if (more && !epan && tid == 96)
       s_pu = CHOL || (T == Tp && !(T & 1) &&
                       ld_acquire(&p.cnt[k * nt + k + 1]) >= need_before(p, k, k + 1, k));
-    tile_store<CHOL>(D, dk, ld, T, rk, p.solve + static_cast<long long>(k) * kSolveSlot);
+    tile_store<CHOL, NC>(D, dk, ld, T, rk, p.solve + static_cast<long long>(k) * kSolveSlot);
     // publish: the CTA barrier orders every thread's stores before thread 0's
     // release reduction (cumulative), so one fence instead of one per warp.
     // A failing pivot (factor_block8, warp 0) raised s_fail before DIAG's last
     // barrier: no global read of the status word on the chain.
-    __syncthreads();
-    const bool pan = more && s_pl && s_pu;
+    csync<NW>();
+    if (PUB) {  // hand D(k) to the publisher (release of tile (k,k))
+      if (tid == 0) {
+        __threadfence_block();
+        s_dready = k;
+      }
+      if (s_fail) return;  // the publisher raises the abort flag
+    }
+    const bool pan = more && (epan || (s_pl && s_pu));
     pref = more && s_pf;
-    if (warp > 0 && (pan || pref)) {  // (warp 0 issues none: thread 0's fence below)
+    if (warp > 0 && ((pan && !epan) || pref)) {  // (warp 0 issues none: thread 0's fence below)
       const int hp = T >> 1, t7 = tid - 32;
-      if (pan) {
+      if (pan && !epan) {
         const double* al = p.a + static_cast<long long>(kT + T) * ld + kT;
-        for (int e = t7; e < T * hp; e += kThreads - 32) {
+        for (int e = t7; e < T * hp; e += NC - 32) {
           const int i = e / hp, c = 2 * (e - i * hp);
           cp_async16(Lt + i * kNP + c, al + static_cast<long long>(i) * ld + c);
           if (!CHOL) cp_async16(Ut + i * kNP + c, dk + T + static_cast<long long>(i) * ld + c);
@@ -1481,29 +1573,31 @@ __device__ void walker(const Params& p, double* dsm) {
       }
       if (pref) {
         const double* dn = dk + static_cast<long long>(T) * ld + T;
-        for (int e = t7; e < T * hp; e += kThreads - 32) {
+        for (int e = t7; e < T * hp; e += NC - 32) {
           const int i = e / hp, c = 2 * (e - i * hp);
           cp_async16(P + i * kNP + c, dn + static_cast<long long>(i) * ld + c);
         }
       }
       cp_async_commit();
     }
-    if (tid == 0) {
-      const bool f = s_fail != 0;
-      s_ok = !f;
-      if (f)
-        atomicExch(p.abort, 1);
-      else
-        red_release_add(&p.cnt[k * nt + k], k >= 1 ? 2 * T : T);  // stage k-1 + DIAG(k)
+    if (!PUB) {
+      if (tid == 0) {
+        const bool f = s_fail != 0;
+        s_ok = !f;
+        if (f)
+          atomicExch(p.abort, 1);
+        else
+          red_release_add(&p.cnt[k * nt + k], k >= 1 ? 2 * T : T);  // stage k-1 + DIAG(k)
+      }
+      csync<NW>();
+      if (!s_ok) return;
     }
-    __syncthreads();
-    if (!s_ok) return;
     if (!more) break;
     // ---- first tiles of the panel: L(k+1,k) = A(k+1,k) U11^-1, U(k,k+1) = L11^-1 A(k,k+1)
     if (pan) {
       cp_async_wait<0>();
       stamp(k, 4);
-      for (int e = tid; e < NF * 64; e += kThreads) {  // inverses for the second solve (below)
+      for (int e = tid; e < NF * 64; e += NC) {  // inverses for the second solve (below)
         const int b = e >> 6, ii = (e >> 3) & 7, c = e & 7;
         const double v = inv[512 + b * 64 + c * 8 + ii];
         invX[e] = CHOL ? v * (8 * b + c < T ? rk[8 * b + c] : 1.0) : v;
@@ -1517,11 +1611,11 @@ __device__ void walker(const Params& p, double* dsm) {
       const double* au = dk + T;
       // element pairs (16-byte loads; T even keeps every pair aligned, T odd
       // loads the odd tail element alone)
-      constexpr int kHP = Tp / 2, kPer = (Tp * kHP + kThreads - 1) / kThreads;
+      constexpr int kHP = Tp / 2, kPer = (Tp * kHP + NC - 1) / NC;
       double2 vl[kPer], vu[kPer];
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
-        const int e = tid + u * kThreads, x = e / kHP, y = 2 * (e - x * kHP);
+        const int e = tid + u * NC, x = e / kHP, y = 2 * (e - x * kHP);
         const bool in = e < Tp * kHP && x < T && y < T;
         vl[u] = vu[u] = make_double2(0.0, 0.0);
         if (in && !(T & 1)) {
@@ -1541,14 +1635,14 @@ __device__ void walker(const Params& p, double* dsm) {
       // entries of M between 8-blocks are read, and D is identity-padded
       // block inverses of the second M: LU inv(L_bb^T) = inv(L_bb)^T;
       // Cholesky inv(diag(l) L_bb^T) = inv(L_bb)^T diag(1/l)
-      for (int e = tid; e < NF * 64; e += kThreads) {
+      for (int e = tid; e < NF * 64; e += NC) {
         const int b = e >> 6, ii = (e >> 3) & 7, c = e & 7;
         const double v = inv[512 + b * 64 + c * 8 + ii];
         invX[e] = CHOL ? v * (8 * b + c < T ? rk[8 * b + c] : 1.0) : v;
       }
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
-        const int e = tid + u * kThreads, x = e / kHP, y = 2 * (e - x * kHP);
+        const int e = tid + u * NC, x = e / kHP, y = 2 * (e - x * kHP);
         if (e < Tp * kHP) {
           *reinterpret_cast<double2*>(Lt + x * kNP + y) = vl[u];
           if (!CHOL) *reinterpret_cast<double2*>(Ut + x * kNP + y) = vu[u];
@@ -1556,7 +1650,7 @@ __device__ void walker(const Params& p, double* dsm) {
       }
     }
     }  // panel not prefetched
-    __syncthreads();
+    csync<NW>();
     stamp(k, 6);
     // warps 0..3: L21 strips (X * M = A21); warps 4..7: U12 strips on the
     // transposed view (X * L11^T = A12^T)
@@ -1575,14 +1669,14 @@ __device__ void walker(const Params& p, double* dsm) {
         }
       }
     }
-    __syncthreads();
+    csync<NW>();
     stamp(k, 7);
-    {  // publish the solved tiles
+    {  // the solved tiles -> global
       double* gl = p.a + static_cast<long long>(kT + T) * ld + kT;
       double* gu = dk + T;
       if (!(T & 1)) {  // 16-byte stores of element pairs
         constexpr int kHP = Tp / 2;
-        for (int e = tid; e < Tp * kHP; e += kThreads) {
+        for (int e = tid; e < Tp * kHP; e += NC) {
           const int x = e / kHP, y = 2 * (e - x * kHP);
           if (x < T && y < T) {
             *reinterpret_cast<double2*>(gl + static_cast<long long>(x) * ld + y) =
@@ -1593,17 +1687,22 @@ __device__ void walker(const Params& p, double* dsm) {
           }
         }
       } else {
-        for (int e = tid; e < T * T; e += kThreads) {
+        for (int e = tid; e < T * T; e += NC) {
           const int x = e / T, y = e - x * T;
           gl[static_cast<long long>(x) * ld + y] = Lt[x * kNP + y];
           if (!CHOL) gu[static_cast<long long>(x) * ld + y] = Ut[x * kNP + y];
         }
       }
     }
-    __syncthreads();
+    csync<NW>();
     if (tid == 0) {
-      red_release_add(&p.cnt[(k + 1) * nt + k], T);
-      if (!CHOL) red_release_add(&p.cnt[k * nt + k + 1], T);
+      if (PUB) {  // the publisher releases them
+        __threadfence_block();
+        s_luready = k;
+      } else {
+        red_release_add(&p.cnt[(k + 1) * nt + k], T);
+        if (!CHOL) red_release_add(&p.cnt[k * nt + k + 1], T);
+      }
     }
     stamp(k, 5);
   }
