@@ -2325,8 +2325,11 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // walker + urgent-queue workers + bulk-queue workers
   {
+    // measured (tools/gpu_knobs2.sh): with >= 80 panel steps the bulk queue
+    // is the bound in the early steps and 4 urgent CTAs beat 8 (Cholesky XL
+    // 1.83 -> 1.81 ms, LU XL 3.07 -> 3.01 ms); LU N=2000 (50 steps) wants 6-8
     const char* v = std::getenv("TT_DAG_URGENT_CTAS");
-    const int want = v ? std::atoi(v) : 8;
+    const int want = v ? std::atoi(v) : (nt >= 80 ? 4 : 8);
     w->nuw = nurg > 0 ? std::max(1, std::min(want, sms / 2)) : 0;
   }
   const int nbulk = w->ntasks - nurg;
@@ -2398,11 +2401,12 @@ cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long l
   }();
   prm.pipe = w.pipe;  // fixed at create(): the chunk depth's shared-memory budget depends on it
   prm.d = w.chunk;
-  // measured default: Cholesky (whose bulk GEMMs feed the next step's strips
-  // directly) gains 2% from publishing each strip at once, LU does not
-  prm.eager_sig = [chol] {
+  // measured default: publishing each GEMM strip right after its stores
+  // (round 1: Cholesky +2%; round 2, 4 urgent CTAs: LU XL 3.01 -> 2.94 ms,
+  // LU N=2000 neutral)
+  prm.eager_sig = [] {
     const char* v = std::getenv("TT_DAG_EAGER_SIGNAL");
-    return v ? std::atoi(v) : (chol ? 1 : 0);
+    return v ? std::atoi(v) : 1;
   }();
   prm.solve = w.solve;
   const int nf = (bx + 7) / 8;
