@@ -1271,7 +1271,7 @@ __device__ __forceinline__ void tile_store(const double* D, double* __restrict__
 // 8 columns: R_b = S_b - X_<b * M_<b,b (DMMA), X_b = R_b * inv(M_bb) (DMMA).
 // MMODE: 0 = M[r][c] = Ms[r*kNP + c]; 1 = M[r][c] = Ms[c*kNP + r] (M is the
 // transpose of the stored tile); 2 = as 1, scaled by msc[r] (Cholesky L^T).
-template <int NF, bool SMEM = false, int MMODE = 0>
+template <int NF, bool SMEM = false, int MMODE = 0, int MF = kMF>
 __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long rs, long long cs,
                                           int nrows, int T, const double* __restrict__ Ms,
                                           const double* __restrict__ Minv,
@@ -1280,9 +1280,9 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
   // global row strips: element pairs as 16-byte accesses when aligned
   const bool vec = !SMEM && cs == 1 && !(rs & 1) && !(T & 1) &&
                    !(reinterpret_cast<uintptr_t>(base) & 15);
-  double ra[NF][kMF][2];
+  double ra[NF][MF][2];
 #pragma unroll
-  for (int mf = 0; mf < kMF; ++mf) {
+  for (int mf = 0; mf < MF; ++mf) {
     const int r = mf * 8 + g;
     const bool rv = r < nrows;
     const double* row = base + static_cast<long long>(rv ? r : 0) * rs;
@@ -1317,9 +1317,9 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
   // X_b M_bc terms in ascending b, the same order as the left-looking form.
 #pragma unroll
   for (int b = 0; b < NF; ++b) {
-    double rf[kMF][2];
+    double rf[MF][2];
 #pragma unroll
-    for (int mf = 0; mf < kMF; ++mf) {
+    for (int mf = 0; mf < MF; ++mf) {
       const double v0 = __shfl_sync(0xffffffffu, ra[b][mf][0], src0);
       const double v1 = __shfl_sync(0xffffffffu, ra[b][mf][1], src0);
       const double w0 = __shfl_sync(0xffffffffu, ra[b][mf][0], src1);
@@ -1327,17 +1327,17 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
       rf[mf][0] = odd ? v1 : v0;
       rf[mf][1] = odd ? w1 : w0;
     }
-    double xo[kMF][2] = {};
+    double xo[MF][2] = {};
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const double m = Minv[b * 64 + (4 * s + t) * 8 + g];
 #pragma unroll
-      for (int mf = 0; mf < kMF; ++mf) dmma_8x8x4(xo[mf][0], xo[mf][1], rf[mf][s], m);
+      for (int mf = 0; mf < MF; ++mf) dmma_8x8x4(xo[mf][0], xo[mf][1], rf[mf][s], m);
     }
     if (b + 1 < NF) {
-      double xa[kMF][2];  // -X_b in A-fragment layout
+      double xa[MF][2];  // -X_b in A-fragment layout
 #pragma unroll
-      for (int mf = 0; mf < kMF; ++mf) {
+      for (int mf = 0; mf < MF; ++mf) {
         const double v0 = __shfl_sync(0xffffffffu, xo[mf][0], src0);
         const double v1 = __shfl_sync(0xffffffffu, xo[mf][1], src0);
         const double w0 = __shfl_sync(0xffffffffu, xo[mf][0], src1);
@@ -1353,11 +1353,11 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
           double m = MMODE == 0 ? Ms[mr * kNP + mc] : Ms[mc * kNP + mr];
           if (MMODE == 2) m *= msc[mr];
 #pragma unroll
-          for (int mf = 0; mf < kMF; ++mf) dmma_8x8x4(ra[c][mf][0], ra[c][mf][1], xa[mf][s], m);
+          for (int mf = 0; mf < MF; ++mf) dmma_8x8x4(ra[c][mf][0], ra[c][mf][1], xa[mf][s], m);
         }
     }
 #pragma unroll
-    for (int mf = 0; mf < kMF; ++mf) {
+    for (int mf = 0; mf < MF; ++mf) {
       const int r = mf * 8 + g;
       if (r < nrows) {
         double* row = base + static_cast<long long>(r) * rs;
@@ -1654,7 +1654,14 @@ __device__ void walker(const Params& p, double* dsm) {
     stamp(k, 6);
     // warps 0..3: L21 strips (X * M = A21); warps 4..7: U12 strips on the
     // transposed view (X * L11^T = A12^T)
-    {
+    if (CHOL && NF <= NW) {
+      // Cholesky (T <= 8 NW): 8-row strips, one per compute warp — the serial
+      // chain over the 8-column blocks carries half the work per block of a
+      // 16-row strip (measured 2.5 us for three 16-row strips)
+      const int c0 = warp * 8;
+      if (c0 < T)
+        warp_trsm<NF, true, 2, 1>(Lt + c0 * kNP, kNP, 1, min(8, T - c0), T, D, invX, rk + 64);
+    } else {
       const int sw = warp & 3;
       const int c0 = sw * kStrip;
       if (c0 < T) {
