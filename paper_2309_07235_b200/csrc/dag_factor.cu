@@ -1661,6 +1661,17 @@ __device__ void walker(const Params& p, double* dsm) {
       const int c0 = warp * 8;
       if (c0 < T)
         warp_trsm<NF, true, 2, 1>(Lt + c0 * kNP, kNP, 1, min(8, T - c0), T, D, invX, rk + 64);
+    } else if (!CHOL && NF <= 5) {
+      // LU (T <= 40): L21 on 8-row strips (warps 0-4), U12 on 16-row strips
+      // of the transposed view (warps 5-7)
+      if (warp < 5) {
+        const int c0 = warp * 8;
+        if (c0 < T)
+          warp_trsm<NF, true, 0, 1>(Lt + c0 * kNP, kNP, 1, min(8, T - c0), T, D, inv);
+      } else {
+        const int c0 = (warp - 5) * kStrip;
+        if (c0 < T) warp_trsm<NF, true, 1>(Ut + c0, 1, kNP, min(kStrip, T - c0), T, D, invX);
+      }
     } else {
       const int sw = warp & 3;
       const int c0 = sw * kStrip;
