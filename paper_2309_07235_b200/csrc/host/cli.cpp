@@ -328,6 +328,14 @@ int cmd_tune(const Args& a) {
   } else {
     char err[512] = {0};
     if (batch != static_cast<int>(devices.size())) {  // --batch K: K evaluators over the devices
+      // K > devices puts several timed evaluators on one GPU: their event
+      // windows overlap (the persistent kernel fills the GPU), so the runtimes
+      // the tuner learns are contended — a functional-test mode, said so here
+      if (batch > static_cast<int>(devices.size()))
+        std::fprintf(stderr,
+                     "warning: --batch %d > %zu device(s): evaluators share a GPU and time each "
+                     "other's kernels (functional-test mode, not a tuning measurement)\n",
+                     batch, devices.size());
       std::vector<int> d;
       for (int i = 0; i < batch; ++i) d.push_back(devices[i % devices.size()]);
       devices = d;
