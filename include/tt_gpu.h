@@ -169,6 +169,14 @@ int tt_dag_tile(int n, int by, int bx);
  * max(128, 5120 / T) rows (adjacent by-row regions per task); -1 when the
  * graph schedule runs. */
 int tt_dag_region_rows(int n, int by, int bx);
+/* DMMA GEMM (3mm, graph-schedule updates), host-side introspection: the CTA
+ * region a knob region (fy, fx) of an m x n product maps to and the tile
+ * variant that sweeps it — out = {reg_y, reg_x, bm, bn, consumer warps}.
+ * Knob edges in [32, 128] are kept; smaller ones are packed (floor(64 / f)
+ * knob regions per CTA region), larger ones split into equal parts <= 128
+ * (replaces the reference's matmul_tiled outer loops, kernels.cpp:91-111).
+ * Needs no device. */
+int tt_gemm_plan(int m, int n, int fy, int fx, int* out);
 /* Number of leading tasks of that list forming the urgent queue (the rest is
  * the bulk queue); -1 when the graph schedule runs instead. */
 int tt_dag_urgent(int kernel, int n, int by, int bx);

@@ -27,7 +27,7 @@ EXPORTS = (
     "tt_get_input", "tt_residual", "tt_dev_lu", "tt_dev_cholesky", "tt_dev_mm3",
     "tt_dev_gemm", "tt_dev_fill_uniform", "tt_launch_count", "tt_build_info", "tt_dag_tasks",
     "tt_dag_trace", "tt_dag_urgent", "tt_dag_chunk_depth", "tt_dag_tile", "tt_dag_region_rows",
-    "tt_lu_factor_batch", "tt_cholesky_factor_batch",
+    "tt_lu_factor_batch", "tt_cholesky_factor_batch", "tt_gemm_plan",
 )
 
 _lib = None
@@ -77,6 +77,7 @@ def load() -> ctypes.CDLL:
         "tt_dag_chunk_depth": (c_int, [c_int, c_int, c_int]),
         "tt_dag_tile": (c_int, [c_int, c_int, c_int]),
         "tt_dag_region_rows": (c_int, [c_int, c_int, c_int]),
+        "tt_gemm_plan": (c_int, [c_int, c_int, c_int, c_int, ctypes.c_void_p]),
         "tt_lu_factor_batch": (c_int, [vp, vp, c_int, c_int, c_int, c_int, c_int_p]),
         "tt_cholesky_factor_batch": (c_int, [vp, vp, c_int, c_int, c_int, c_int, c_int_p]),
     }
@@ -120,6 +121,14 @@ def dag_tile(n: int, by: int, bx: int) -> int | None:
     """Tile T the persistent schedule runs for (n, by, bx), None on the graph schedule."""
     t = load().tt_dag_tile(n, by, bx)
     return None if t < 0 else int(t)
+
+
+def gemm_plan(m: int, n: int, fy: int, fx: int) -> dict:
+    """CTA region and tile variant a 3mm knob region (fy, fx) maps to (tt_gemm_plan)."""
+    out = (ctypes.c_int * 5)()
+    if load().tt_gemm_plan(m, n, fy, fx, ctypes.cast(out, ctypes.c_void_p)):
+        raise ValueError("gemm_plan: invalid arguments")
+    return {"reg_y": out[0], "reg_x": out[1], "bm": out[2], "bn": out[3], "warps": out[4]}
 
 
 def dag_region_rows(n: int, by: int, bx: int) -> int | None:

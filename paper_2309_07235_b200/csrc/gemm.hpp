@@ -49,6 +49,8 @@ struct GemmPlan {
   long long grid() const { return static_cast<long long>(nreg_y) * nreg_x; }
 };
 GemmPlan plan_gemm(int M, int N, int fy, int fx);
+// DMMA consumer warps of the BM x BN variant (GemmShape<BM, BN>::NCW).
+int consumer_warps(int bm, int bn);
 
 // C (+)= (+/-) A * B on `stream`.  c points at the output view origin.
 // lower: write only view elements with i + diag_off >= j (Cholesky).

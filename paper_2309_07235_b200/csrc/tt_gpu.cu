@@ -1032,6 +1032,17 @@ int tt_dag_region_rows(int n, int by, int bx) {
   return tt::dag::region_rows(by, tt::dag::tile_for(n, bx));
 }
 
+int tt_gemm_plan(int m, int n, int fy, int fx, int* out) {
+  if (m < 1 || n < 1 || fy < 1 || fx < 1 || !out) return TT_EINVAL;
+  const tt::GemmPlan p = tt::plan_gemm(m, n, fy, fx);
+  out[0] = p.reg_y;
+  out[1] = p.reg_x;
+  out[2] = p.bm;
+  out[3] = p.bn;
+  out[4] = tt::consumer_warps(p.bm, p.bn);
+  return TT_OK;
+}
+
 int tt_dag_urgent(int kernel, int n, int by, int bx) {
   if (!tt::dag::eligible(n, by, bx)) return -1;
   int nu = 0;

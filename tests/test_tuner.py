@@ -145,3 +145,19 @@ def test_batch_ask_one_fit_per_batch_is_fast():
     dt = time.perf_counter() - t0
     assert len(got) == 8
     assert dt < 0.2, dt  # one fit + 2048-point scoring for 8 candidates
+
+
+def test_batch_ask_distinct_and_spreads_over_model_cells():
+    """k > 1 BayesOpt: one candidate per forest cell first (candidates with equal
+    (mean, sd) are indistinguishable to the model); the batch is distinct, untaken
+    and inside the space."""
+    t = tuning.Tuner("bayesopt", "3mm", "extralarge", 3)
+    rng = np.random.default_rng(1)
+    seen = set()
+    for _ in range(12):
+        got = t.ask_batch(8)
+        assert len(got) == 8 and len(set(got)) == 8
+        assert not (set(got) & seen)
+        seen |= set(got)
+        for f in got:
+            t.tell(f, float(rng.random()))
