@@ -483,8 +483,8 @@ def schedule_info(lib, kid, n, by, bx):
 
 EXTRA_CASES = [
     # (name, kernel case args, config, flops, how the config was chosen)
-    ("lu_large_fixed_block", ("lu", 2000), (400, 40), lu_flops(2000),
-     "configs[1]: fixed block, the fastest of the N=2000 knob sweep (profiles/sweep_lu2000_r02.jsonl)"),
+    ("lu_large_fixed_block", ("lu", 2000), (500, 40), lu_flops(2000),
+     "configs[1]: fixed block, the fastest of the N=2000 knob sweep on the final kernel (profiles/lu2000sweep_r02c.txt)"),
     ("lu_extralarge", ("lu", 4000), (4000, 40), lu_flops(4000),
      "best of the N=4000 knob sweep on the final kernel (profiles/xlsweep_r02c.txt)"),
     ("mm3_large_fixed_tile", ("3mm", 800, 900, 1000, 1100, 1200), (100, 40, 1000, 300, 16, 120),
