@@ -1581,16 +1581,15 @@ __device__ void walker(const Params& p, double* dsm) {
       cp_async_commit();
     }
     if (!PUB) {
+      // s_fail is visible to every thread since the barrier above: no second
+      // barrier here, warp 0's release fence overlaps the other warps' panel work
       if (tid == 0) {
-        const bool f = s_fail != 0;
-        s_ok = !f;
-        if (f)
+        if (s_fail)
           atomicExch(p.abort, 1);
         else
           red_release_add(&p.cnt[k * nt + k], k >= 1 ? 2 * T : T);  // stage k-1 + DIAG(k)
       }
-      csync<NW>();
-      if (!s_ok) return;
+      if (s_fail) return;
     }
     if (!more) break;
     // ---- first tiles of the panel: L(k+1,k) = A(k+1,k) U11^-1, U(k,k+1) = L11^-1 A(k,k+1)
