@@ -1432,7 +1432,7 @@ __device__ void walker(const Params& p, double* dsm) {
   constexpr bool PUB = CHOL && NF <= 6;  // measured: Cholesky XL -1%, LU +3% (7 compute warps)
   constexpr int NW = PUB ? kWarps - 1 : kWarps;  // compute warps
   constexpr int NC = NW * 32;
-  __shared__ int s_ok, s_pf, s_pl, s_pu, s_fail, s_el, s_eu;
+  __shared__ int s_ok, s_pf, s_pl, s_pu, s_fail;
   __shared__ volatile int s_dready, s_luready, s_wabort;
   if (tid == 0) {
     s_fail = 0;
@@ -1503,35 +1503,8 @@ __device__ void walker(const Params& p, double* dsm) {
       }
       csync<NW>();
     }
-    // Early panel copy (PUB): if the panel inputs A(k+1,k) (and A(k,k+1)) are
-    // final already, warp 2 (and warp 3) copy them into Lt (Ut) now, under
-    // DIAG(k) (step k-1's panel tiles were stored before the step began).
-    const bool try_early = PUB && k + 1 < nt && T == Tp && !(T & 1);
-    if (try_early && (warp == 2 || (!CHOL && warp == 3))) {
-      const bool lo = warp == 2;
-      int ok = 0;
-      if (lane == 0)
-        ok = lo ? ld_acquire(&p.cnt[(k + 1) * nt + k]) >= need_before(p, k, k, k)
-                : ld_acquire(&p.cnt[k * nt + k + 1]) >= need_before(p, k, k + 1, k);
-      ok = __shfl_sync(0xffffffffu, ok, 0);
-      if (ok) {
-        const int hp = T >> 1;
-        const double* src = lo ? p.a + static_cast<long long>(kT + T) * ld + kT : dk + T;
-        double* dst = lo ? Lt : Ut;
-        for (int e = lane; e < T * hp; e += 32) {
-          const int i = e / hp, c = 2 * (e - i * hp);
-          cp_async16(dst + i * kNP + c, src + static_cast<long long>(i) * ld + c);
-        }
-        cp_async_commit();
-      }
-      if (lane == 0) {
-        if (lo) s_el = ok;
-        else s_eu = ok;
-      }
-    }
     stamp(k, 2);
     diag_blocked<CHOL, NW>(D, T, kT, p.info, inv, rk, &s_fail);
-    const bool epan = try_early && s_el && (CHOL || s_eu);  // (after DIAG's barriers)
     stamp(k, 3);
     // Polls next to the tile store (warps 1-3, one lane each): the panel inputs
     // A(k+1,k) (and A(k,k+1)) at stage k-1, and the next diagonal tile at
@@ -1541,9 +1514,9 @@ __device__ void walker(const Params& p, double* dsm) {
     const bool more = k + 1 < nt;
     if (more && tid == 32)
       s_pf = !(T & 1) && ld_acquire(&p.cnt[(k + 1) * nt + k + 1]) >= need_before(p, k + 1, k + 1, k);
-    if (more && !epan && tid == 64)
+    if (more && tid == 64)
       s_pl = T == Tp && !(T & 1) && ld_acquire(&p.cnt[(k + 1) * nt + k]) >= need_before(p, k, k, k);
-    if (more && !epan && tid == 96)
+    if (more && tid == 96)
       s_pu = CHOL || (T == Tp && !(T & 1) &&
                       ld_acquire(&p.cnt[k * nt + k + 1]) >= need_before(p, k, k + 1, k));
     tile_store<CHOL, NC>(D, dk, ld, T, rk, p.solve + static_cast<long long>(k) * kSolveSlot);
@@ -1559,11 +1532,11 @@ __device__ void walker(const Params& p, double* dsm) {
       }
       if (s_fail) return;  // the publisher raises the abort flag
     }
-    const bool pan = more && (epan || (s_pl && s_pu));
+    const bool pan = more && s_pl && s_pu;
     pref = more && s_pf;
-    if (warp > 0 && ((pan && !epan) || pref)) {  // (warp 0 issues none: thread 0's fence below)
+    if (warp > 0 && (pan || pref)) {  // (warp 0 issues none: thread 0's fence below)
       const int hp = T >> 1, t7 = tid - 32;
-      if (pan && !epan) {
+      if (pan) {
         const double* al = p.a + static_cast<long long>(kT + T) * ld + kT;
         for (int e = t7; e < T * hp; e += NC - 32) {
           const int i = e / hp, c = 2 * (e - i * hp);
