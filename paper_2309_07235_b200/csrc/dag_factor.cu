@@ -1183,6 +1183,19 @@ __device__ __forceinline__ void csync() {
   else
     asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
 }
+// The same barrier, AND-reducing a predicate over the participating threads.
+template <int NW>
+__device__ __forceinline__ bool csync_and(bool pred) {
+  if (NW == kWarps) return __syncthreads_and(pred);
+  int r;
+  asm volatile(
+      "{\n .reg .pred p, q;\n setp.ne.s32 p, %1, 0;\n"
+      " bar.red.and.pred q, 1, %2, p;\n selp.s32 %0, 1, 0, q;\n}"
+      : "=r"(r)
+      : "r"(pred ? 1 : 0), "n"(NW * 32)
+      : "memory");
+  return r != 0;
+}
 
 // Blocked elimination of the tile in shared memory with look-ahead: while
 // warps 1..7 apply step b's trailing update, warp 0 updates the next
@@ -1374,6 +1387,19 @@ __device__ __forceinline__ void warp_trsm(double* __restrict__ base, long long r
   }
 }
 
+// Shared-memory step counters of the walker hand-off: release store / acquire
+// load at CTA scope (the PTX pattern for a flag protecting prior writes).
+__device__ __forceinline__ void st_release_cta(volatile int* f, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_u32(const_cast<int*>(f))), "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(volatile int* f) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(const_cast<int*>(f)))
+               : "memory");
+  return v;
+}
+
 // ---------------------------------------------------------------- walker
 // The walker's publisher warp (tiles <= 48, see walker): the compute warps
 // store the factored diagonal tile and the solved panel tiles themselves (224
@@ -1392,11 +1418,10 @@ __device__ void walker_publisher(const Params& p, const int* sfail, volatile int
   if ((threadIdx.x & 31) != 0) return;
   const int T = p.T, nt = p.nt;
   auto await = [&](volatile int* f, int k) -> bool {
-    while (*f < k) {
+    while (ld_acquire_cta(f) < k) {
       if (*wabort) return false;
       __nanosleep(32);
     }
-    __threadfence_block();
     return true;
   };
   for (int k = 0; k < nt; ++k) {
@@ -1432,7 +1457,7 @@ __device__ void walker(const Params& p, double* dsm) {
   constexpr bool PUB = CHOL && NF <= 6;  // measured: Cholesky XL -1%, LU +3% (7 compute warps)
   constexpr int NW = PUB ? kWarps - 1 : kWarps;  // compute warps
   constexpr int NC = NW * 32;
-  __shared__ int s_ok, s_pf, s_pl, s_pu, s_fail;
+  __shared__ int s_pf, s_pl, s_pu, s_fail;
   __shared__ volatile int s_dready, s_luready, s_wabort;
   if (tid == 0) {
     s_fail = 0;
@@ -1445,13 +1470,15 @@ __device__ void walker(const Params& p, double* dsm) {
     return;
   }
   bool pref = false;  // tile (k,k) of this step was prefetched into P (stages < k-1)
-  auto wait1 = [&](const int* c, int need) -> bool {  // compute warps
+  // Thread 0 waits on one counter (or two: c2 != nullptr); the barrier
+  // AND-reduces its verdict (no shared status word to race on).
+  auto wait1 = [&](const int* c, int need, const int* c2 = nullptr, int need2 = 0) -> bool {
+    bool ok = true;
     if (tid == 0) {
-      s_ok = wait_ge(p, c, need);
-      if (!s_ok) s_wabort = 1;  // the publisher stops too
+      ok = wait_ge(p, c, need) && (!c2 || wait_ge(p, c2, need2));
+      if (!ok) s_wabort = 1;  // the publisher stops too
     }
-    csync<NW>();
-    return s_ok;
+    return csync_and<NW>(ok);
   };
   auto stamp = [&](int k, int i) {
     if (p.trace && tid == 0)
@@ -1527,8 +1554,7 @@ __device__ void walker(const Params& p, double* dsm) {
     csync<NW>();
     if (PUB) {  // hand D(k) to the publisher (release of tile (k,k))
       if (tid == 0) {
-        __threadfence_block();
-        s_dready = k;
+        st_release_cta(&s_dready, k);
       }
       if (s_fail) return;  // the publisher raises the abort flag
     }
@@ -1575,8 +1601,9 @@ __device__ void walker(const Params& p, double* dsm) {
         invX[e] = CHOL ? v * (8 * b + c < T ? rk[8 * b + c] : 1.0) : v;
       }
     } else {
-    if (!wait1(&p.cnt[(k + 1) * nt + k], need_before(p, k, k, k))) return;
-    if (!CHOL && !wait1(&p.cnt[k * nt + k + 1], need_before(p, k, k + 1, k))) return;
+    if (!wait1(&p.cnt[(k + 1) * nt + k], need_before(p, k, k, k),
+               CHOL ? nullptr : &p.cnt[k * nt + k + 1], need_before(p, k, k + 1, k)))
+      return;
     stamp(k, 4);
     {
       const double* al = p.a + static_cast<long long>(kT + T) * ld + kT;
@@ -1687,8 +1714,7 @@ __device__ void walker(const Params& p, double* dsm) {
     csync<NW>();
     if (tid == 0) {
       if (PUB) {  // the publisher releases them
-        __threadfence_block();
-        s_luready = k;
+        st_release_cta(&s_luready, k);
       } else {
         red_release_add(&p.cnt[(k + 1) * nt + k], T);
         if (!CHOL) red_release_add(&p.cnt[k * nt + k + 1], T);
