@@ -150,15 +150,17 @@ __device__ bool wait_ge(const Params& p, const int* addr, int need) {
         if (it >= (1 << 20) && dt > kWatchdogNs) {
           // first expiring waiter records what it waited for (diagnostics:
           // CTA, counter index, target, last value seen)
-          if (atomicCAS(p.abort + 2, 0, 1) == 0) {
-            p.abort[3] = blockIdx.x;
-            p.abort[4] = static_cast<int>(addr - p.cnt);
-            p.abort[5] = need;
-            p.abort[6] = ld_relaxed(addr);
-            p.abort[7] = ld_relaxed(p.next);      // urgent queue position
-            p.abort[8] = ld_relaxed(p.next + 2);  // bulk queue position
-            p.abort[9] = it;                          // polls
-            p.abort[10] = static_cast<int>(dt / 1000000);  // ms waited
+          if (atomicCAS(p.abort + 3, 0, 1) == 0) {
+            p.abort[4] = blockIdx.x;
+            p.abort[5] = static_cast<int>(addr - p.cnt);
+            p.abort[6] = need;
+            p.abort[7] = ld_relaxed(addr);
+            p.abort[8] = ld_relaxed(p.next);      // urgent queue position
+            p.abort[9] = ld_relaxed(p.next + 2);  // bulk queue position
+            p.abort[10] = it;                         // polls
+            p.abort[11] = static_cast<int>(dt / 1000000);  // ms waited
+            p.abort[12] = ld_relaxed(p.abort + 2);    // CTAs of this launch that started
+            p.abort[13] = gridDim.x;
           }
           atomicExch(p.abort, 2);
           atomicMin(p.info, kTimeout);
@@ -1744,6 +1746,7 @@ __global__ void __launch_bounds__(kThreads, 1) dag_kernel(Params p) {
   };
   const long long ld = p.ld;
   const int4 kNone = make_int4(-1, 0, 0, 0);
+  if (tid == 0) atomicAdd(p.abort + 2, 1);  // CTAs started (watchdog diagnostics)
 
   if (blockIdx.x == 0) {
     if (!p.nodeps) walker<NF, CHOL>(p, dsm);
@@ -2317,9 +2320,9 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   w->pipe = pipe_gemm() ? 1 : 0;
   w->nsteps = nt;
   // nt*nt tile counters, then: urgent next, abort flag, bulk next, and the
-  // watchdog record {recorded, cta, counter, need, seen, urgent pos, bulk pos, polls, ms}
-  // (kDiagInts)
-  w->cnt_bytes = (static_cast<size_t>(nt) * nt + 3 + kDiagInts) * sizeof(int);
+  // started-CTA count, and the watchdog record {recorded, cta, counter, need, seen,
+  // urgent pos, bulk pos, polls, ms, started, grid} (kDiagInts)
+  w->cnt_bytes = (static_cast<size_t>(nt) * nt + 4 + kDiagInts) * sizeof(int);
   cudaError_t e = cudaMalloc(&w->tasks, tasks.size() * sizeof(int4));
   if (e != cudaSuccess) return e;
   e = cudaMemcpy(w->tasks, tasks.data(), tasks.size() * sizeof(int4), cudaMemcpyHostToDevice);
@@ -2357,15 +2360,15 @@ std::string watchdog_info(const Workspace& w) {
   if (!w.cnt) return {};
   const int nt = w.nsteps;
   int rec[kDiagInts] = {};
-  if (cudaMemcpy(rec, w.cnt + static_cast<size_t>(nt) * nt + 3, sizeof(rec),
+  if (cudaMemcpy(rec, w.cnt + static_cast<size_t>(nt) * nt + 4, sizeof(rec),
                  cudaMemcpyDeviceToHost) != cudaSuccess || rec[0] == 0)
     return {};
   char buf[256];
   std::snprintf(buf, sizeof(buf),
                 "cta %d waited on tile (%d, %d) for %d rows, saw %d (T %d; queue positions: "
-                "urgent %d of %d, bulk %d of %d; %d polls, %d ms)",
+                "urgent %d of %d, bulk %d of %d; %d polls, %d ms; %d of %d CTAs started)",
                 rec[1], rec[2] / nt, rec[2] % nt, rec[3], rec[4], w.T, rec[5], w.nurgent, rec[6],
-                w.ntasks - w.nurgent, rec[7], rec[8]);
+                w.ntasks - w.nurgent, rec[7], rec[8], rec[9], rec[10]);
   return buf;
 }
 
@@ -2386,9 +2389,10 @@ cudaError_t enqueue(const Workspace& w, bool chol, double* a, int n, long long l
   }();
   const size_t tiles = static_cast<size_t>(nt) * nt * sizeof(int);
   cudaError_t e = cudaMemsetAsync(w.cnt, nodeps ? 0x3F : 0, tiles, s);
-  // queue positions and the abort flag; the watchdog record after them is
-  // kept across launches (zeroed at create): it names the first timeout
-  if (e == cudaSuccess) e = cudaMemsetAsync(w.cnt + static_cast<size_t>(nt) * nt, 0, 3 * sizeof(int), s);
+  // queue positions, the abort flag and the started-CTA count; the watchdog
+  // record after them is kept across launches (zeroed at create): it names the
+  // first timeout
+  if (e == cudaSuccess) e = cudaMemsetAsync(w.cnt + static_cast<size_t>(nt) * nt, 0, 4 * sizeof(int), s);
   if (e != cudaSuccess) return e;
   Params prm;
   prm.a = a;

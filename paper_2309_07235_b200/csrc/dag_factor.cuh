@@ -83,7 +83,7 @@ constexpr long long kMaxTasks = 8LL << 20;
 constexpr long long kWatchdogNs = 4000000000LL;
 constexpr int kTimeout = -2147483647 - 1;  // INT_MIN
 // Ints after the abort flag kept for the watchdog record (see watchdog_info).
-constexpr int kDiagInts = 9;
+constexpr int kDiagInts = 11;
 
 
 // Opts every persistent-kernel variant into its shared memory on the

@@ -252,6 +252,8 @@ int get_graph(tt_ctx* ctx, const GraphKey& key, Enqueue&& enq, cudaGraphExec_t* 
     return cuda_fail(ctx, e, "schedule capture");
   }
   TT_CUDA(ctx, e2, "cudaStreamEndCapture");
+  if (const char* dot = std::getenv("TT_GRAPH_DOT"))  // debug aid: the captured graph
+    cudaGraphDebugDotPrint(graph, dot, cudaGraphDebugDotFlagsVerbose);
   cudaGraphExec_t exec = nullptr;
   e = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
