@@ -2353,6 +2353,15 @@ cudaError_t create(Workspace* w, bool chol, int n, int by, int bx) {
   }
   const int nbulk = w->ntasks - nurg;
   w->grid = 1 + w->nuw + std::max(0, std::min(sms - 1 - w->nuw, nbulk));
+  // The uploads and the memset above run on the legacy default stream, which
+  // does not order with the context's non-blocking stream: a pageable
+  // cudaMemcpy may return before its DMA lands and cudaMemset is asynchronous.
+  // Without this wait the first launch of a new workspace could read task
+  // descriptors or counters that were still being written (long knob sweeps
+  // saw rare watchdog aborts with counters zeroed under a running schedule,
+  // and one illegal address).
+  e = cudaStreamSynchronize(cudaStreamLegacy);
+  if (e != cudaSuccess) return e;
   return cudaSuccess;
 }
 

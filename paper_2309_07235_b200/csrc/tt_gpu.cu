@@ -545,7 +545,10 @@ int tt_ctx_create(int device, tt_ctx** out) {
       cudaMalloc(&ctx->ws, sizeof(double) * tt::kIB * tt::kIB) != cudaSuccess ||
       cudaMalloc(&ctx->red, 2 * sizeof(unsigned long long)) != cudaSuccess)
     return cleanup(TT_ENOMEM);
-  if (cudaMemset(ctx->info, 0x7F, sizeof(int)) != cudaSuccess) return cleanup(TT_EDEVICE);
+  // (legacy default stream: wait, so it cannot land after work on ctx->stream)
+  if (cudaMemset(ctx->info, 0x7F, sizeof(int)) != cudaSuccess ||
+      cudaStreamSynchronize(cudaStreamLegacy) != cudaSuccess)
+    return cleanup(TT_EDEVICE);
   // Set the dynamic-smem attribute of every GEMM variant up front (so graph
   // capture never meets a first-use attribute call).
   for (int bt = 0; bt < 2; ++bt)
